@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Hamming decoder (BASELINE.json metric: coded Gbit/s
+decoded, device-timed, max over ranks, plus % of HBM peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Default workload = BASELINE.json configs[4] ("C5"): (63,57) codewords, 2^39
+coded bits (64 GiB) in total, sharded by codeword range across the ranks
+(total fixed -> "scaling": "strong"; --weak keeps 64 GiB per rank).  It fits
+one B200 (~131 GB of buffers), so N=1 runs the whole of it.  One step = one
+pass of the hot path over the rank's shard (hamming_decode: syndrome,
+correction, redundancy removal, packing, syndromes, count) plus, for N > 1,
+the NCCL all_reduce of the 8-byte corrected count.  Inputs are generated on
+the device by the library's seeded channel generator (p = 0.1 single-bit
+errors) and are far larger than L2, so no flush is needed.
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
+paper-derived checker, as it stands) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+SEED = 0x14126862
+FALLBACK_HBM_GBS = 6650.0
+
+CONFIGS = {
+    # name: (m, total coded bits or bytes rule, p, q2, description)
+    "c5": dict(m=6, coded_bits=1 << 39, p=0.1, q2=0.0,
+               desc="C5: Hamming(63,57), 2^39 coded bits (64 GiB) aggregate, sharded by codeword range"),
+    "c3m6": dict(m=6, coded_bits=(256 << 20) * 8, p=0.1, q2=0.0, desc="C3: Hamming(63,57), 256 MiB packet"),
+    "c3m5": dict(m=5, coded_bits=(256 << 20) * 8, p=0.1, q2=0.0, desc="C3: Hamming(31,26), 256 MiB packet"),
+    "c3m4": dict(m=4, coded_bits=(256 << 20) * 8, p=0.1, q2=0.0, desc="C3: Hamming(15,11), 256 MiB packet"),
+    "c3m3": dict(m=3, coded_bits=(256 << 20) * 8, p=0.1, q2=0.0, desc="C3: Hamming(7,4), 256 MiB packet"),
+    "c4": dict(m=5, coded_bits=(1 << 30) * 8, p=0.1, q2=0.25, desc="C4: Hamming(31,26), 1 GiB, p=0.1, q2=0.25"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", mp
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+# ------------------------------------------------------------------ clocks
+REASON_FIELDS = ["clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+                 "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap",
+                 "clocks_event_reasons.hw_power_brake_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join(REASON_FIELDS)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 2 + len(REASON_FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(REASON_FIELDS, r[2:]):
+                if val.lower() == "active":
+                    reasons.add(name.split(".")[-1])
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- cpu baseline
+def cpu_oracle_run(m: int, p: float, q2: float, n_cw: int, threads: int):
+    """Time the CPU oracle (as it stands) decoding a seeded sample of the
+    workload with `threads` host threads.  Returns (seconds, result)."""
+    import oracle
+    oracle.build()
+    rx, _, _ = oracle.generate(m, SEED, 0, n_cw, p=p, q2=q2, threads=threads)
+    t0 = time.perf_counter()
+    res = oracle.decode_mt(m, rx, n_cw, threads)
+    return time.perf_counter() - t0, res
+
+
+def cpu_baseline(m, p, q2, threads, target_s=1.0):
+    n = (1 << m) - 1
+    probe = 1 << 15
+    t, _ = cpu_oracle_run(m, p, q2, probe, threads)
+    n_cw = int(min(1 << 26, max(probe, probe * target_s / max(t, 1e-6)))) // 1024 * 1024
+    t, _ = cpu_oracle_run(m, p, q2, n_cw, threads)
+    gbps = n * n_cw / t / 1e9
+    return {"value": round(gbps, 4), "unit": "coded Gbit/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {n_cw} codewords of the workload (same m, p, q2, seed), {n * n_cw / 8 / 2**20:.0f} MiB "
+                      f"coded, decoded by the plain C oracle on {threads} host threads in {t:.2f} s "
+                      f"({t * threads:.0f} CPU-s)"}
+
+
+# ------------------------------------------------------------------- main
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    ap.add_argument("--coded-gib", type=float, default=None, help="override total coded size (GiB)")
+    ap.add_argument("--weak", action="store_true", help="keep the per-rank size fixed instead of the total")
+    ap.add_argument("--no-syndromes", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-gib", type=float, default=8.0, help="host-buffer e2e packet size (GiB coded)")
+    return ap.parse_args()
+
+
+def workload(args, world):
+    cfg = dict(CONFIGS[args.config])
+    m = cfg["m"]
+    n = (1 << m) - 1
+    bits = cfg["coded_bits"] if args.coded_gib is None else int(args.coded_gib * (1 << 30) * 8)
+    if args.weak:
+        bits *= world
+    N = bits // n
+    return cfg, m, n, N
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    cfg, m, n, N = workload(args, world)
+    threads = len(os.sched_getaffinity(0))
+    # each step decodes a bounded sample sized so the whole run takes ~minutes
+    probe = 1 << 15
+    t, _ = cpu_oracle_run(m, cfg["p"], cfg["q2"], probe, threads)
+    total_steps = args.steps + args.warmup
+    n_cw = int(max(probe, probe * min(20.0, 120.0 / total_steps) / max(t, 1e-6))) // 1024 * 1024
+    import oracle
+    rx, _, _ = oracle.generate(m, SEED, 0, n_cw, p=cfg["p"], q2=cfg["q2"], threads=threads)
+    for _ in range(args.warmup):
+        oracle.decode_mt(m, rx, n_cw, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.decode_mt(m, rx, n_cw, threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = n * n_cw / (ms / 1e3) / 1e9
+    sample = (f"{n_cw} codewords ({n * n_cw / 8 / 2**20:.0f} MiB coded) of the workload per step, plain C oracle "
+              f"on {threads} host threads")
+    out = {
+        "impl": "reference", "metric": "coded Gbit/s decoded (device-timed, max over ranks)", "value": round(value, 4),
+        "unit": "coded Gbit/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded counter-based channel, oracle generator)",
+        "config": {"workload": cfg["desc"], "m": m, "n_codewords": N, "p": cfg["p"], "q2": cfg["q2"],
+                   "parallelism": "host threads", "sample_codewords": n_cw},
+        "cpu_baseline": {"value": round(value, 4), "unit": "coded Gbit/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "coded Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1412_6862_b200 as ham
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg, m, n, N = workload(args, world)
+    k = n - m
+    c0, c1 = ham.shard_range(N, rank, world)
+    n_loc = c1 - c0
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs: generated on the device, keyed by the global codeword index
+    rx = ham.channel_generate(m, SEED, c0, n_loc, p=cfg["p"], q2=cfg["q2"], device=dev)
+    data = torch.empty(max(1, ham.data_bytes(m, n_loc)), dtype=torch.uint8, device=dev)
+    syn = None if args.no_syndromes else torch.empty(max(1, n_loc), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        ham.decode(m, rx, n_loc, data_out=data, syndromes=syn if syn is not None else False, corrected=cnt)
+        if world > 1:
+            dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    launches_per_step = ham.last_launch_count()
+    grid = ham.last_grid_blocks()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_end = torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev_start.record(stream)
+    for i in range(args.steps):
+        kev[i][0].record(stream)
+        ham.decode(m, rx, n_loc, data_out=data, syndromes=syn if syn is not None else False, corrected=cnt)
+        kev[i][1].record(stream)
+        if world > 1:
+            dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    ev_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_ms = ev_start.elapsed_time(ev_end)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    t_tensor = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
+    t_ms, k_ms = float(t_tensor[0]), float(t_tensor[1])
+    ms_per_step = t_ms / args.steps
+    total_bits = n * N
+    value = total_bits / (ms_per_step / 1e3) / 1e9  # coded Gbit/s, whole job
+
+    # roofline of the decode kernel (per rank): algorithmic bytes per launch
+    alg_bytes = ham.coded_bytes(m, n_loc) + ham.data_bytes(m, n_loc) + (0 if syn is None else n_loc) + 8
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    peak, peak_src, mp = measured_peaks()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            key = f"m{m}_{'syn' if syn is not None else 'nosyn'}"
+            if key in pj:
+                traffic = round(pj[key]["traffic_per_alg_byte"] * alg_bytes)
+        except Exception:
+            traffic = None
+
+    result = {
+        "metric": "coded Gbit/s decoded (device-timed, max over ranks)",
+        "value": round(value, 2), "unit": "coded Gbit/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: seeded counter-based channel on the device (uniform data, p=%g single-bit errors, q2=%g)"
+                % (cfg["p"], cfg["q2"]),
+        "config": {"workload": cfg["desc"], "m": m, "n": n, "k": k, "n_codewords": N,
+                   "n_codewords_per_rank": n_loc, "p": cfg["p"], "q2": cfg["q2"],
+                   "syndromes": syn is not None, "parallelism": f"dp{world} (codeword-range shards)",
+                   "l2": "inputs larger than L2 (no flush needed)", "grid_blocks": grid},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": f"tiles_kernel<DecodeOp<{m}>> (+1 tail warp) per hamming_decode call",
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(k_ms, 4), "peak_source": peak_src},
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+
+    # ---- e2e: the same metric through the public host-buffer C-ABI call
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank)
+    del rx, data, syn
+    torch.cuda.empty_cache()
+
+    if rank == 0 and not args.no_cpu:
+        try:
+            result["cpu_baseline"] = cpu_baseline(m, cfg["p"], cfg["q2"], len(os.sched_getaffinity(0)))
+        except Exception as e:  # the oracle is a reported baseline only
+            result["cpu_baseline"] = {"value": None, "unit": "coded Gbit/s", "error": str(e)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank):
+    """Host packet (pinned) -> hamming_decode_host (pipelined H2D / decode /
+    D2H on 3 streams) -> host data, syndromes and count; timed by wall clock
+    around the synchronous call, max over ranks."""
+    import torch.distributed as dist
+    N_e = int(args.e2e_gib * (1 << 30) * 8) // n
+    c0, c1 = ham.shard_range(N_e, rank, world)
+    n_loc = c1 - c0
+    rx_d = ham.channel_generate(m, SEED, c0, n_loc, p=cfg["p"], q2=cfg["q2"], device=dev)
+    rx_h = torch.empty(ham.coded_bytes(m, n_loc), dtype=torch.uint8, pin_memory=True)
+    rx_h.copy_(rx_d[: rx_h.numel()])
+    del rx_d
+    data_h = torch.empty(ham.data_bytes(m, n_loc), dtype=torch.uint8, pin_memory=True)
+    syn_h = torch.empty(n_loc, dtype=torch.uint8, pin_memory=True)
+    chunk = 1 << 22
+    ws = torch.empty(ham.host_workspace_bytes(m, chunk, 3, True), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    ham.decode_host(m, rx_h, n_loc, data_h, syn_h, ws, chunk_codewords=chunk, n_streams=3)
+    steps = max(1, min(args.steps, 3))
+    ts = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ham.decode_host(m, rx_h, n_loc, data_h, syn_h, ws, chunk_codewords=chunk, n_streams=3)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt[0])
+    out = {"value": round(n * N_e / t / 1e9, 2), "unit": "coded Gbit/s",
+           "h2d_bytes_per_step": ham.coded_bytes(m, n_loc),
+           "d2h_bytes_per_step": ham.data_bytes(m, n_loc) + n_loc + 8,
+           "workload": f"{args.e2e_gib:g} GiB coded packet of the same code/channel in pinned host memory, "
+                       f"hamming_decode_host (chunk {chunk} codewords, 3 streams), wall clock per call",
+           "steps": steps, "ms_per_step": round(t * 1e3, 2)}
+    del rx_h, data_h, syn_h, ws
+    return out
+
+
+if __name__ == "__main__":
+    main()

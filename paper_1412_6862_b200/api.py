@@ -1,0 +1,172 @@
+"""Python binding of the C ABI (include/hamming.h), same names, on torch CUDA
+tensors.  torch supplies device memory and streams only; every step of the
+decode runs in libhamming.so's sm_100a kernels.
+
+Readings of the paper used by the layout (R3, R4): LSB-first
+packed streams; codeword c = stream bits [c*n, c*n + n); data bits of c at
+[c*k, c*k + k).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from ._lib import check, lib
+
+TILE = 1024  # codewords per warp tile of the decode kernel
+
+
+def code_nk(m: int) -> tuple[int, int]:
+    if not 2 <= m <= 6:
+        raise ValueError("m must be in [2, 6]")
+    n = (1 << m) - 1
+    return n, n - m
+
+
+def coded_bytes(m: int, n_codewords: int) -> int:
+    return int(lib().hamming_coded_bytes(m, n_codewords))
+
+
+def data_bytes(m: int, n_codewords: int) -> int:
+    return int(lib().hamming_data_bytes(m, n_codewords))
+
+
+def channel_thresholds(p: float, q2: float) -> tuple[int, int, int]:
+    """(thresh, all, q2thresh) of the synthetic channel: an error event iff
+    u < floor(p 2^64) (all codewords when p >= 1); weight 2 iff
+    hi32(u) < floor(q2 2^32)."""
+    if not (0.0 <= p <= 1.0 and 0.0 <= q2 <= 1.0):
+        raise ValueError("p and q2 must lie in [0, 1]")
+    all_ = 1 if p >= 1.0 else 0
+    return (0 if all_ else int(p * 2.0 ** 64)), all_, int(q2 * 2.0 ** 32)
+
+
+def _dev_ptr(t: Optional[torch.Tensor], name: str, min_bytes: int):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() * t.element_size() < min_bytes:
+        raise ValueError(f"{name} holds {t.numel() * t.element_size()} bytes, needs {min_bytes}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream, device) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+@dataclass
+class DecodeResult:
+    data: torch.Tensor                  # uint8 [data_bytes(m, N)]
+    syndromes: Optional[torch.Tensor]   # uint8 [N] or None
+    corrected: torch.Tensor             # int64 [1], device-resident count
+
+
+def hamming_decode(m: int, rx: torch.Tensor, n_codewords: int, *, data_out: Optional[torch.Tensor] = None,
+                   syndromes: bool | torch.Tensor = True, corrected: Optional[torch.Tensor] = None,
+                   stream: Optional[torch.cuda.Stream] = None) -> DecodeResult:
+    """Decode `n_codewords` (2^m-1, 2^m-1-m) codewords of the packed packet
+    `rx` (uint8 CUDA tensor) -- include/hamming.h `hamming_decode`."""
+    code_nk(m)
+    N = int(n_codewords)
+    dev = rx.device
+    if data_out is None:
+        data_out = torch.empty(max(1, data_bytes(m, N)), dtype=torch.uint8, device=dev)
+    if syndromes is True:
+        syn = torch.empty(max(1, N), dtype=torch.uint8, device=dev)
+    elif syndromes is False or syndromes is None:
+        syn = None
+    else:
+        syn = syndromes
+    if corrected is None:
+        corrected = torch.empty(1, dtype=torch.int64, device=dev)
+    st = lib().hamming_decode(m, _dev_ptr(rx, "rx", coded_bytes(m, N)), N,
+                              _dev_ptr(data_out, "data_out", data_bytes(m, N)),
+                              _dev_ptr(syn, "syndromes", N), _dev_ptr(corrected, "corrected", 8),
+                              _stream_handle(stream, dev))
+    check(st, "hamming_decode")
+    return DecodeResult(data_out, syn, corrected)
+
+
+decode = hamming_decode
+
+
+def hamming_encode(m: int, data: torch.Tensor, n_codewords: int, *, rx_out: Optional[torch.Tensor] = None,
+                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    code_nk(m)
+    N = int(n_codewords)
+    if rx_out is None:
+        rx_out = torch.empty(max(1, coded_bytes(m, N)), dtype=torch.uint8, device=data.device)
+    st = lib().hamming_encode(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
+                              _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)), _stream_handle(stream, data.device))
+    check(st, "hamming_encode")
+    return rx_out
+
+
+encode = hamming_encode
+
+
+def hamming_channel_generate(m: int, seed: int, c_first: int, n_codewords: int, p: float = 0.1, q2: float = 0.0,
+                             *, rx_out: Optional[torch.Tensor] = None, device=None,
+                             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Seeded synthetic received packet on the GPU."""
+    code_nk(m)
+    N = int(n_codewords)
+    thresh, all_, q2t = channel_thresholds(p, q2)
+    if rx_out is None:
+        rx_out = torch.empty(max(1, coded_bytes(m, N)), dtype=torch.uint8,
+                             device=device if device is not None else "cuda")
+    st = lib().hamming_channel_generate(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
+                                        _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)),
+                                        _stream_handle(stream, rx_out.device))
+    check(st, "hamming_channel_generate")
+    return rx_out
+
+
+channel_generate = hamming_channel_generate
+
+
+def host_workspace_bytes(m: int, chunk_codewords: int, n_streams: int, with_syndromes: bool) -> int:
+    return int(lib().hamming_host_workspace_bytes(m, chunk_codewords, n_streams, int(with_syndromes)))
+
+
+def hamming_decode_host(m: int, rx_host: torch.Tensor, n_codewords: int, data_host: torch.Tensor,
+                        syndromes_host: Optional[torch.Tensor], workspace: torch.Tensor,
+                        chunk_codewords: int = 1 << 24, n_streams: int = 3) -> int:
+    """End-to-end decode of a HOST packet (pinned CPU tensors) through the
+    library's pipelined H2D / decode / D2H path (P:L113-132 ADT).  Returns the
+    corrected count."""
+    code_nk(m)
+    N = int(n_codewords)
+    for t, name in ((rx_host, "rx_host"), (data_host, "data_host"), (syndromes_host, "syndromes_host")):
+        if t is not None and (t.is_cuda or not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CPU tensor")
+    if rx_host.numel() < coded_bytes(m, N) or data_host.numel() < data_bytes(m, N):
+        raise ValueError("host buffers too small")
+    if syndromes_host is not None and syndromes_host.numel() < N:
+        raise ValueError("syndromes_host too small")
+    cnt = ctypes.c_ulonglong(0)
+    st = lib().hamming_decode_host(m, ctypes.c_void_p(rx_host.data_ptr()), N, ctypes.c_void_p(data_host.data_ptr()),
+                                   None if syndromes_host is None else ctypes.c_void_p(syndromes_host.data_ptr()),
+                                   ctypes.byref(cnt), _dev_ptr(workspace, "workspace", 1), chunk_codewords,
+                                   n_streams)
+    check(st, "hamming_decode_host")
+    return int(cnt.value)
+
+
+decode_host = hamming_decode_host
+
+
+def last_launch_count() -> int:
+    return int(lib().hamming_last_launch_count())
+
+
+def last_grid_blocks() -> int:
+    return int(lib().hamming_last_grid_blocks())

@@ -1,0 +1,848 @@
+// paper_1412_6862_b200/csrc/hamming.cu -- sm_100a kernels + C ABI (include/hamming.h).
+//
+// Hot path: per-codeword Hamming decode of a bit-packed
+// packet of concatenated perfect (2^m-1, 2^m-1-m) codewords -- the paper's
+// checksum kernel (Algorithm 1) and error kernel (ED, EC, RR)
+// fused into one HBM pass.  B200 design:
+//
+//   * Work unit = a warp tile of 1024 codewords.  Because n and k are odd or
+//     small, 32 codewords of one lane occupy exactly n input words and k output
+//     words (gcd(n, 32) = 1 for odd n), so a warp tile is 128*n input bytes and
+//     128*k output bytes: always 16-byte aligned, always a whole number of words.
+//   * a1 load/unpack: one elected lane moves the tile HBM -> shared memory with a
+//     1-D TMA bulk copy (cp.async.bulk + mbarrier complete_tx), STAGES deep per
+//     warp; each lane then reads its own n words (lane stride n words is odd, so
+//     the reads are bank-conflict free) and extracts codeword c with compile-time
+//     funnel shifts (bit offset c*n - 1 is a constant after unrolling).
+//   * a2 syndrome: one POPC per syndrome bit on the codeword AND the index-set
+//     mask M_j (P:L98 index sets; "modulo 2 (XOR)").  For m = 6 the two
+//     32-bit halves are folded first (positions p and p+32 share their low five
+//     bits), so every mask is 32-bit.
+//   * a3 ED/EC: v ^= 1 << s with the dummy bit 0 standing in for "no error" --
+//     branch free, no divergence (the paper's Fermi divergence problem).
+//   * a4 RR: m-1 shift-and-mask steps (the pext of the data mask).
+//   * a5 merge/pack: each lane ORs its k-bit results into k registers at
+//     compile-time offsets, stores them to shared memory (odd stride again),
+//     and the elected lane writes the whole tile back with one bulk S2G copy.
+//   * a6 syndromes: 32 bytes per lane, two 16-byte streaming stores (the warp
+//     writes 1 KiB contiguous).
+//   * a7 count: per-lane register count -> warp __reduce_add_sync -> block
+//     shared-memory sum -> one 64-bit atomic per CTA.
+//   * Persistent grid: one CTA per SM (or more for small m), each warp runs an
+//     independent grid-stride loop over tiles; no __syncthreads in the loop.
+//
+// The ragged tail (< 1024 codewords) runs the same lane function in a one-warp
+// kernel with bounded, zero-filled loads; it also writes *corrected first so the
+// main kernel can accumulate into it (stream order), i.e. the count is
+// overwritten without a memset.
+//
+// Nothing here is shared with oracle/ (the CPU checker).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "hamming.h"
+
+namespace {
+
+// ------------------------------------------------------------------ geometry
+template <int M>
+struct Geo {
+  static constexpr int n = (1 << M) - 1;
+  static constexpr int k = n - M;
+};
+
+constexpr int kTileCw = 1024;  // codewords per warp tile (32 lanes x 32)
+
+// Parity mask of index set I_j on a register v whose bit p holds position p
+// (bit 0 = dummy), positions 1..min(n, 31).  (I_j = {p : bit j of p}.)
+__host__ __device__ constexpr uint32_t pmask(int n, int j) {
+  uint32_t mk = 0;
+  for (int p = 1; p <= n && p < 32; ++p)
+    if ((p >> j) & 1) mk |= (1u << p);
+  return mk;
+}
+
+// Redundancy removal, group g (positions 2^g+1 .. 2^(g+1)-1): after shifting v
+// right by g+2 the group lands on data bits [2^g-g-1, 2^(g+1)-g-2].
+__host__ __device__ constexpr uint32_t dmask(int g) {
+  return ((1u << ((1 << g) - 1)) - 1u) << ((1 << g) - g - 1);
+}
+
+// --------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "HAM_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra HAM_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 1-D TMA: global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+// 1-D TMA: shared -> global, bulk-group completion.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void st_global_cs_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+// ------------------------------------------------- compile-time bit plumbing
+// Read `width` (<= 32) bits starting at lane-stream bit b from the register
+// array w[0..NW); bits past the array read as 0.  b is a constant after unrolling.
+template <int NW>
+__device__ __forceinline__ uint32_t take_bits(const uint32_t (&w)[NW], int b) {
+  const int q = b >> 5, r = b & 31;
+  const uint32_t a = (q < NW) ? w[q] : 0u;
+  if (r == 0) return a;
+  const uint32_t c = (q + 1 < NW) ? w[q + 1] : 0u;
+  return __funnelshift_r(a, c, r);
+}
+// OR a clean `width`-bit value into the register array o at lane-stream bit b.
+template <int NO>
+__device__ __forceinline__ void put_bits(uint32_t (&o)[NO], int b, uint32_t val, int width) {
+  const int q = b >> 5, r = b & 31;
+  o[q] |= val << r;
+  if (r != 0 && r + width > 32) o[q + 1] |= val >> (32 - r);
+}
+
+// --------------------------------------------------------- per-codeword math
+// Decode one codeword given as v = (lo, hi): bit p of v holds position p
+// (hi bit i = position 32 + i; hi unused for m <= 5).  Returns the syndrome s
+// and the corrected data bits (dlo: data bits 0.., dhi for m = 6:
+// data bits 26..56).
+template <int M>
+__device__ __forceinline__ uint32_t decode_cw(uint32_t lo, uint32_t hi, uint32_t& dlo, uint32_t& dhi) {
+  constexpr int n = Geo<M>::n;
+  uint32_t s;
+  if constexpr (M <= 5) {
+    s = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) s |= static_cast<uint32_t>(__popc(lo & pmask(n, j)) & 1) << j;  // a2
+    lo ^= 1u << s;                                                                               // a3
+    uint32_t d = 0;
+#pragma unroll
+    for (int g = 1; g < M; ++g) d |= (lo >> (g + 2)) & dmask(g);  // a4
+    dlo = d;
+    dhi = 0;
+  } else {
+    const uint32_t x = lo ^ hi;  // fold: positions p and p+32 agree in bits 0..4
+    s = static_cast<uint32_t>(__popc(hi) & 1) << 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) s |= static_cast<uint32_t>(__popc(x & pmask(31, j)) & 1) << j;
+    const uint64_t f = 1ull << s;
+    lo ^= static_cast<uint32_t>(f);
+    hi ^= static_cast<uint32_t>(f >> 32);
+    uint32_t d = 0;
+#pragma unroll
+    for (int g = 1; g < 5; ++g) d |= (lo >> (g + 2)) & dmask(g);
+    dlo = d;        // data bits 0..25 (positions 3..31)
+    dhi = hi >> 1;  // data bits 26..56 (positions 33..63)
+  }
+  return s;
+}
+
+// Encode one message (dlo, dhi as produced by decode_cw) into v = (lo, hi):
+// data at non-power-of-two positions, parity 2^j = XOR over I_j \ {2^j}.
+template <int M>
+__device__ __forceinline__ void encode_cw(uint32_t dlo, uint32_t dhi, uint32_t& lo, uint32_t& hi) {
+  constexpr int n = Geo<M>::n;
+  constexpr int G = (M <= 5) ? M : 5;
+  uint32_t v = 0;
+#pragma unroll
+  for (int g = 1; g < G; ++g) v |= (dlo & dmask(g)) << (g + 2);
+  uint32_t h = (M == 6) ? (dhi << 1) : 0u;
+  uint32_t s = 0;
+  if constexpr (M <= 5) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) s |= static_cast<uint32_t>(__popc(v & pmask(n, j)) & 1) << j;
+  } else {
+    const uint32_t x = v ^ h;
+    s = static_cast<uint32_t>(__popc(h) & 1) << 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) s |= static_cast<uint32_t>(__popc(x & pmask(31, j)) & 1) << j;
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) v |= ((s >> j) & 1u) << (1 << j);
+  if constexpr (M == 6) h |= (s >> 5) & 1u;
+  lo = v;
+  hi = h;
+}
+
+// Emit codeword v (bit p = position p) as stream bits [b, b+n).
+template <int M, int NO>
+__device__ __forceinline__ void put_codeword(uint32_t (&o)[NO], int b, uint32_t lo, uint32_t hi) {
+  constexpr int n = Geo<M>::n;
+  if constexpr (M <= 4) {
+    put_bits(o, b, (lo >> 1) & ((1u << n) - 1u), n);
+  } else if constexpr (M == 5) {
+    put_bits(o, b, lo >> 1, 31);
+  } else {
+    put_bits(o, b, (lo >> 1) | (hi << 31), 32);
+    put_bits(o, b + 32, hi >> 1, 31);
+  }
+}
+
+// ------------------------------------------------------------ tile operators
+// Each operator processes the 32 codewords of one lane: `in` = the lane's
+// IN_W input words, `out` = its OUT_W output words (both in shared memory),
+// `side` = 8 words of per-codeword bytes (syndromes), returns a count.
+// `valid` = number of the lane's 32 codewords that exist (32 except in the tail).
+
+template <int M>
+struct DecodeOp {
+  static constexpr int IN_W = Geo<M>::n;
+  static constexpr int OUT_W = Geo<M>::k;
+  static constexpr int IN_BITS = Geo<M>::n;  // per codeword
+  static constexpr bool HAS_SIDE = true;
+  struct Args {};
+
+  __device__ __forceinline__ static uint32_t lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                  uint32_t (&side)[8], uint64_t /*cw0*/, int /*valid*/,
+                                                  const Args&) {
+    constexpr int n = Geo<M>::n, k = Geo<M>::k;
+    uint32_t w[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) w[i] = in[i];
+    uint32_t o[k];
+#pragma unroll
+    for (int i = 0; i < k; ++i) o[i] = 0;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      uint32_t lo, hi = 0;
+      if (c == 0) {  // v = w << 1 (no previous codeword: dummy bit 0 = 0)
+        lo = w[0] << 1;
+        if constexpr (M == 6) hi = __funnelshift_l(w[0], w[1], 1);
+      } else {       // v = lane-stream bits [c*n - 1, c*n - 1 + 32*(1 or 2))
+        lo = take_bits(w, c * n - 1);
+        if constexpr (M == 6) hi = take_bits(w, c * n + 31);
+      }
+      uint32_t dlo, dhi;
+      const uint32_t s = decode_cw<M>(lo, hi, dlo, dhi);
+      if constexpr (M <= 5) {
+        put_bits(o, c * k, dlo, k);
+      } else {
+        put_bits(o, c * k, dlo, 26);
+        put_bits(o, c * k + 26, dhi, 31);
+      }
+      side[c >> 2] |= s << (8 * (c & 3));
+      cnt += (s != 0);
+    }
+#pragma unroll
+    for (int i = 0; i < k; ++i) out[i] = o[i];
+    return cnt;
+  }
+};
+
+template <int M>
+struct EncodeOp {
+  static constexpr int IN_W = Geo<M>::k;
+  static constexpr int OUT_W = Geo<M>::n;
+  static constexpr int IN_BITS = Geo<M>::k;
+  static constexpr bool HAS_SIDE = false;
+  struct Args {};
+
+  __device__ __forceinline__ static uint32_t lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                  uint32_t (&)[8], uint64_t, int, const Args&) {
+    constexpr int n = Geo<M>::n, k = Geo<M>::k;
+    uint32_t w[k];
+#pragma unroll
+    for (int i = 0; i < k; ++i) w[i] = in[i];
+    uint32_t o[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      uint32_t dlo, dhi = 0;
+      if constexpr (M <= 5) {
+        dlo = take_bits(w, c * k);
+        if constexpr (k < 32) dlo &= (1u << k) - 1u;
+      } else {
+        dlo = take_bits(w, c * k) & ((1u << 26) - 1u);
+        dhi = take_bits(w, c * k + 26) & 0x7FFFFFFFu;
+      }
+      uint32_t lo, hi;
+      encode_cw<M>(dlo, dhi, lo, hi);
+      put_codeword<M>(o, c * n, lo, hi);
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) out[i] = o[i];
+    return 0;
+  }
+};
+
+// splitmix64 output function (Steele, Lea & Flood 2014) -- written here
+// independently of oracle/oracle.c; the two are compared byte for byte.
+__device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <int M>
+struct GenerateOp {
+  static constexpr int IN_W = 0;
+  static constexpr int OUT_W = Geo<M>::n;
+  static constexpr int IN_BITS = 0;
+  static constexpr bool HAS_SIDE = false;
+  struct Args {
+    uint64_t seed, c_first, thresh, q2thresh;
+    int all;
+  };
+
+  __device__ __forceinline__ static uint32_t lane(const uint32_t*, uint32_t* __restrict__ out, uint32_t (&)[8],
+                                                  uint64_t cw0, int valid, const Args& a) {
+    constexpr int n = Geo<M>::n, k = Geo<M>::k;
+    constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+    uint32_t o[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint64_t g = a.c_first + cw0 + c;
+      const uint64_t base = a.seed + 4 * g * kGamma;
+      const uint64_t u0 = sm64_mix(base + 1 * kGamma);
+      const uint64_t u1 = sm64_mix(base + 2 * kGamma);
+      const uint64_t u2 = sm64_mix(base + 3 * kGamma);
+      const uint64_t u3 = sm64_mix(base + 4 * kGamma);
+      uint32_t dlo, dhi = 0;
+      if constexpr (M <= 5) {
+        dlo = static_cast<uint32_t>(u0) & ((1u << k) - 1u);
+      } else {
+        dlo = static_cast<uint32_t>(u0) & ((1u << 26) - 1u);
+        dhi = static_cast<uint32_t>(u0 >> 26) & 0x7FFFFFFFu;
+      }
+      uint32_t lo, hi;
+      encode_cw<M>(dlo, dhi, lo, hi);
+      const bool ev = a.all || (u1 < a.thresh);
+      const bool two = (u2 >> 32) < a.q2thresh;
+      const uint32_t p1 = 1u + __umulhi(static_cast<uint32_t>(u3), static_cast<uint32_t>(n));
+      uint32_t p2 = p1 + __umulhi(static_cast<uint32_t>(u3 >> 32), static_cast<uint32_t>(n - 1));  // (p1-1)+1+x
+      p2 = (p2 >= static_cast<uint32_t>(n) ? p2 - n : p2) + 1u;
+      uint64_t f = ev ? (1ull << p1) : 0ull;
+      f ^= (ev && two) ? (1ull << p2) : 0ull;
+      lo ^= static_cast<uint32_t>(f);
+      hi ^= static_cast<uint32_t>(f >> 32);
+      if (c >= valid) {  // past the end of the packet (tail only): emit zeros
+        lo = 0;
+        hi = 0;
+      }
+      put_codeword<M>(o, c * n, lo, hi);
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) out[i] = o[i];
+    return 0;
+  }
+};
+// ------------------------------------------------------------------ kernels
+template <class Op>
+struct TileBytes {
+  static constexpr int IN = Op::IN_W * 128;   // 32 lanes x IN_W words x 4 B
+  static constexpr int OUT = Op::OUT_W * 128;
+};
+
+// Persistent warp-tile pipeline: each warp owns STAGES input buffers (TMA bulk
+// loads, mbarrier-tracked) and 2 output buffers (TMA bulk stores).
+template <class Op, int WARPS, int STAGES>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
+                 uint64_t n_tiles, unsigned long long* __restrict__ counter, typename Op::Args args) {
+  constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
+  constexpr int WARP_SMEM = STAGES * IN + 2 * OUT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ unsigned long long block_cnt;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wbase = smem + warp * WARP_SMEM;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * WARP_SMEM) + warp * STAGES;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+  const uint64_t pol = policy_evict_first();
+
+  if (threadIdx.x == 0) block_cnt = 0;
+  if constexpr (IN > 0) {
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+      fence_mbar_init();
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s) {
+        const uint64_t t = gw + s * nw;
+        if (t < n_tiles) {
+          mbar_arrive_expect_tx(&bars[s], IN);
+          bulk_g2s(wbase + s * IN, in + t * IN, IN, &bars[s], pol);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  uint32_t cnt = 0;
+  uint32_t it = 0;
+  for (uint64_t t = gw; t < n_tiles; t += nw, ++it) {
+    const int st = static_cast<int>(it % STAGES);
+    if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
+    uint32_t* obuf = reinterpret_cast<uint32_t*>(wbase + STAGES * IN + (it & 1u) * OUT);
+    if (lane == 0) bulk_wait_read<1>();  // the store issued two tiles ago has read obuf
+    __syncwarp();
+    uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
+    cnt += Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args);
+    fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(out + t * OUT, obuf, OUT, pol);
+      bulk_commit();
+      if constexpr (IN > 0) {
+        const uint64_t nt = t + STAGES * nw;
+        if (nt < n_tiles) {
+          mbar_arrive_expect_tx(&bars[st], IN);
+          bulk_g2s(wbase + st * IN, in + nt * IN, IN, &bars[st], pol);
+        }
+      }
+    }
+    if constexpr (Op::HAS_SIDE) {
+      if (side != nullptr) {
+        uint8_t* sp = side + t * kTileCw + lane * 32;
+        st_global_cs_v4(sp, sidew[0], sidew[1], sidew[2], sidew[3]);
+        st_global_cs_v4(sp + 16, sidew[4], sidew[5], sidew[6], sidew[7]);
+      }
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+
+  if (counter != nullptr) {
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    __syncthreads();
+    if (lane == 0 && cnt) atomicAdd(&block_cnt, static_cast<unsigned long long>(cnt));
+    __syncthreads();
+    if (threadIdx.x == 0 && block_cnt) atomicAdd(counter, block_cnt);
+  }
+}
+
+// Ragged tail (fewer than 1024 codewords, possibly 0) in one warp.  Writes
+// *counter = tail count (a store, not an add): launched first on the stream,
+// it is the "overwrite" half of the count contract.
+template <class Op>
+__global__ void __launch_bounds__(32)
+    tail_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
+                uint64_t c0, uint32_t rem, uint64_t in_total, uint64_t out_total,
+                unsigned long long* __restrict__ counter, int accumulate, typename Op::Args args) {
+  constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
+  __shared__ __align__(16) uint32_t ibuf[IN > 0 ? IN / 4 : 1];
+  __shared__ __align__(16) uint32_t obuf[OUT / 4];
+  const int lane = threadIdx.x;
+  uint32_t cnt = 0;
+  if (rem > 0) {
+    if constexpr (IN > 0) {
+      const uint64_t ib0 = c0 * Op::IN_BITS / 8;  // c0 % 1024 == 0: byte aligned
+      const uint64_t nb = in_total - ib0;
+      uint8_t* ib = reinterpret_cast<uint8_t*>(ibuf);
+      for (int i = lane; i < IN; i += 32) ib[i] = (i < nb) ? in[ib0 + i] : 0;
+      __syncwarp();
+      const uint64_t vbits = static_cast<uint64_t>(rem) * Op::IN_BITS;  // zero the input pad bits
+      for (int i = lane; i < IN / 4; i += 32) {
+        const uint64_t b = static_cast<uint64_t>(i) * 32;
+        if (b >= vbits) ibuf[i] = 0;
+        else if (b + 32 > vbits) ibuf[i] &= (1u << (vbits - b)) - 1u;
+      }
+      __syncwarp();
+    }
+    const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
+    uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cnt = Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, c0 + lane * 32, valid, args);
+    __syncwarp();
+    const uint64_t ob0 = c0 / kTileCw * OUT;  // c0 is a whole number of tiles
+    const uint64_t nb = out_total - ob0;
+    const uint8_t* ob = reinterpret_cast<const uint8_t*>(obuf);
+    for (int i = lane; i < nb && i < OUT; i += 32) out[ob0 + i] = ob[i];
+    if constexpr (Op::HAS_SIDE) {
+      if (side != nullptr) {
+        const uint8_t* sb = reinterpret_cast<const uint8_t*>(sidew);
+        for (int c = 0; c < valid; ++c) side[c0 + lane * 32 + c] = sb[c];
+      }
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0 && counter != nullptr) {
+    if (accumulate) {
+      if (cnt) atomicAdd(counter, static_cast<unsigned long long>(cnt));
+    } else {
+      *counter = cnt;
+    }
+  }
+}
+
+// ---------------------------------------------------------- host-side state
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+thread_local int g_grid = 0;
+
+hamming_status set_err(hamming_status s, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return s;
+}
+hamming_status cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+  return HAMMING_E_CUDA;
+}
+
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sm_count[kMaxDev];
+
+int sm_count(int dev) {
+  int v = (dev >= 0 && dev < kMaxDev) ? g_sm_count[dev].load(std::memory_order_relaxed) : 0;
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    if (dev >= 0 && dev < kMaxDev) g_sm_count[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+template <class Op, int WARPS, int STAGES>
+struct Launcher {
+  static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
+  static constexpr size_t SMEM = static_cast<size_t>(WARPS) * (STAGES * IN + 2 * OUT) + WARPS * STAGES * 8;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+
+  static hamming_status run(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t n_cw, uint64_t in_total,
+                            uint64_t out_total, unsigned long long* counter, const typename Op::Args& args,
+                            cudaStream_t stream, bool accumulate = false) {
+    static std::atomic<int> configured[kMaxDev];
+    static std::atomic<int> blocks_per_sm[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    auto kfn = tiles_kernel<Op, WARPS, STAGES>;
+    if (dev < 0 || dev >= kMaxDev || !configured[dev].load(std::memory_order_acquire)) {
+      e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+      int occ = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, WARPS * 32, SMEM);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      if (dev >= 0 && dev < kMaxDev) {
+        blocks_per_sm[dev].store(std::max(1, occ), std::memory_order_relaxed);
+        configured[dev].store(1, std::memory_order_release);
+      }
+    }
+    const int bps = (dev >= 0 && dev < kMaxDev) ? blocks_per_sm[dev].load(std::memory_order_relaxed) : 1;
+    const uint64_t n_tiles = n_cw / kTileCw;
+    const uint64_t c0 = n_tiles * kTileCw;
+    const uint32_t rem = static_cast<uint32_t>(n_cw - c0);
+    int launches = 0;
+    // tail first: it also initialises *counter
+    if (rem > 0 || (counter != nullptr && !accumulate)) {
+      tail_kernel<Op><<<1, 32, 0, stream>>>(in, out, side, c0, rem, in_total, out_total, counter,
+                                            accumulate ? 1 : 0, args);
+      ++launches;
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e, "tail kernel launch");
+    }
+    int grid = 0;
+    if (n_tiles > 0) {
+      const uint64_t want = (n_tiles + WARPS - 1) / WARPS;
+      grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * bps));
+      kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_tiles, counter, args);
+      ++launches;
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e, "tiles kernel launch");
+    }
+    g_launches = launches;
+    g_grid = grid;
+    return HAMMING_OK;
+  }
+};
+
+// Per-m launch shapes: warps per CTA x TMA stages per warp.
+template <int M> struct Shape;
+template <> struct Shape<2> { static constexpr int W = 16, S = 4; };
+template <> struct Shape<3> { static constexpr int W = 16, S = 4; };
+template <> struct Shape<4> { static constexpr int W = 16, S = 4; };
+template <> struct Shape<5> { static constexpr int W = 12, S = 3; };
+template <> struct Shape<6> { static constexpr int W = 7, S = 2; };
+
+bool ranges_overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
+  if (!a || !b || !na || !nb) return false;
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool bits_overflow(int m, uint64_t N) {
+  const uint64_t n = (1ull << m) - 1;
+  return N > (~0ull) / n;
+}
+
+hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
+                               unsigned long long* counter, cudaStream_t st, bool accumulate) {
+  const uint64_t n = (1ull << m) - 1, k = n - m;
+  const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
+  switch (m) {
+#define HAMMING_DECODE_CASE(MM)                                                                          \
+  case MM:                                                                                               \
+    return Launcher<DecodeOp<MM>, Shape<MM>::W, Shape<MM>::S>::run(in, out, syn, N, ib, ob, counter, {}, \
+                                                                   st, accumulate);
+    HAMMING_DECODE_CASE(2)
+    HAMMING_DECODE_CASE(3)
+    HAMMING_DECODE_CASE(4)
+    HAMMING_DECODE_CASE(5)
+    HAMMING_DECODE_CASE(6)
+#undef HAMMING_DECODE_CASE
+  }
+  return set_err(HAMMING_E_INVALID_M, "decode: m must be in [2, 6]");
+}
+
+constexpr uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+struct HostSlotLayout {
+  uint64_t rx, data, syn, slot;
+};
+
+HostSlotLayout host_slot_layout(int m, uint64_t chunk, int with_syn) {
+  const uint64_t n = (1ull << m) - 1, k = n - m;
+  HostSlotLayout L;
+  L.rx = align256((n * chunk + 7) / 8);
+  L.data = align256((k * chunk + 7) / 8);
+  L.syn = with_syn ? align256(chunk) : 0;
+  L.slot = L.rx + L.data + L.syn;
+  return L;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int hamming_abi_version(void) { return HAMMING_ABI_VERSION; }
+
+uint64_t hamming_coded_bytes(int m, uint64_t N) {
+  if (m < 2 || m > 6 || bits_overflow(m, N)) return 0;
+  const uint64_t n = (1ull << m) - 1;
+  return (n * N + 7) / 8;
+}
+
+uint64_t hamming_data_bytes(int m, uint64_t N) {
+  if (m < 2 || m > 6 || bits_overflow(m, N)) return 0;
+  const uint64_t k = (1ull << m) - 1 - m;
+  return (k * N + 7) / 8;
+}
+
+const char* hamming_status_string(hamming_status s) {
+  switch (s) {
+    case HAMMING_OK: return "ok";
+    case HAMMING_E_INVALID_M: return "invalid m (must be 2..6)";
+    case HAMMING_E_NULL: return "required pointer is NULL";
+    case HAMMING_E_MISALIGNED: return "device buffer not 16-byte aligned";
+    case HAMMING_E_OVERLAP: return "input and output buffers overlap";
+    case HAMMING_E_RANGE: return "size or probability out of range";
+    case HAMMING_E_CUDA: return "CUDA error";
+    case HAMMING_E_ARG: return "invalid argument";
+  }
+  return "unknown status";
+}
+
+const char* hamming_last_error(void) { return g_err; }
+int hamming_last_launch_count(void) { return g_launches; }
+int hamming_last_grid_blocks(void) { return g_grid; }
+
+hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_dev, uint8_t* syn_dev,
+                              unsigned long long* corrected_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_decode: m must be in [2, 6]");
+  if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_decode: n * n_codewords overflows");
+  if (corrected_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_decode: corrected is NULL");
+  if (N > 0 && (rx_dev == nullptr || data_dev == nullptr))
+    return set_err(HAMMING_E_NULL, "hamming_decode: rx or data is NULL");
+  if (!aligned16(rx_dev) || !aligned16(data_dev) || !aligned16(syn_dev))
+    return set_err(HAMMING_E_MISALIGNED, "hamming_decode: rx, data and syndromes must be 16-byte aligned");
+  const uint64_t ib = hamming_coded_bytes(m, N), ob = hamming_data_bytes(m, N);
+  const uint64_t sb = syn_dev ? N : 0;
+  if (ranges_overlap(rx_dev, ib, data_dev, ob) || ranges_overlap(rx_dev, ib, syn_dev, sb) ||
+      ranges_overlap(data_dev, ob, syn_dev, sb) || ranges_overlap(rx_dev, ib, corrected_dev, 8) ||
+      ranges_overlap(data_dev, ob, corrected_dev, 8) || ranges_overlap(syn_dev, sb, corrected_dev, 8))
+    return set_err(HAMMING_E_OVERLAP, "hamming_decode: buffers overlap");
+  return decode_dispatch(m, static_cast<const uint8_t*>(rx_dev), N, static_cast<uint8_t*>(data_dev), syn_dev,
+                         corrected_dev, static_cast<cudaStream_t>(stream), false);
+}
+
+hamming_status hamming_encode(int m, const void* data_dev, uint64_t N, void* rx_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_encode: m must be in [2, 6]");
+  if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_encode: n * n_codewords overflows");
+  if (N == 0) return HAMMING_OK;
+  if (data_dev == nullptr || rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_encode: NULL buffer");
+  if (!aligned16(data_dev) || !aligned16(rx_dev))
+    return set_err(HAMMING_E_MISALIGNED, "hamming_encode: buffers must be 16-byte aligned");
+  const uint64_t ib = hamming_data_bytes(m, N), ob = hamming_coded_bytes(m, N);
+  if (ranges_overlap(data_dev, ib, rx_dev, ob)) return set_err(HAMMING_E_OVERLAP, "hamming_encode: overlap");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint8_t* in = static_cast<const uint8_t*>(data_dev);
+  uint8_t* out = static_cast<uint8_t*>(rx_dev);
+  switch (m) {
+#define HAMMING_ENCODE_CASE(MM) \
+  case MM:                      \
+    return Launcher<EncodeOp<MM>, Shape<MM>::W, Shape<MM>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    HAMMING_ENCODE_CASE(2)
+    HAMMING_ENCODE_CASE(3)
+    HAMMING_ENCODE_CASE(4)
+    HAMMING_ENCODE_CASE(5)
+    HAMMING_ENCODE_CASE(6)
+#undef HAMMING_ENCODE_CASE
+  }
+  return set_err(HAMMING_E_INVALID_M, "hamming_encode: m must be in [2, 6]");
+}
+
+hamming_status hamming_channel_generate(int m, uint64_t seed, uint64_t c_first, uint64_t N, uint64_t thresh,
+                                        int all, uint64_t q2thresh, void* rx_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_channel_generate: m must be in [2, 6]");
+  if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_channel_generate: size overflows");
+  if (q2thresh > (1ull << 32)) return set_err(HAMMING_E_RANGE, "hamming_channel_generate: q2thresh > 2^32");
+  if (N == 0) return HAMMING_OK;
+  if (rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_channel_generate: rx is NULL");
+  if (!aligned16(rx_dev)) return set_err(HAMMING_E_MISALIGNED, "hamming_channel_generate: rx misaligned");
+  const uint64_t ob = hamming_coded_bytes(m, N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* out = static_cast<uint8_t*>(rx_dev);
+  switch (m) {
+#define HAMMING_GEN_CASE(MM)                                                                                 \
+  case MM: {                                                                                                 \
+    typename GenerateOp<MM>::Args a{seed, c_first, thresh, q2thresh, all};                                  \
+    return Launcher<GenerateOp<MM>, 4, 1>::run(nullptr, out, nullptr, N, 0, ob, nullptr, a, st);            \
+  }
+    HAMMING_GEN_CASE(2)
+    HAMMING_GEN_CASE(3)
+    HAMMING_GEN_CASE(4)
+    HAMMING_GEN_CASE(5)
+    HAMMING_GEN_CASE(6)
+#undef HAMMING_GEN_CASE
+  }
+  return set_err(HAMMING_E_INVALID_M, "hamming_channel_generate: m must be in [2, 6]");
+}
+
+size_t hamming_host_workspace_bytes(int m, uint64_t chunk_codewords, int n_streams, int with_syndromes) {
+  if (m < 2 || m > 6 || n_streams < 1 || n_streams > 4 || chunk_codewords == 0 ||
+      bits_overflow(m, chunk_codewords))
+    return 0;
+  return static_cast<size_t>(256 + n_streams * host_slot_layout(m, chunk_codewords, with_syndromes).slot);
+}
+
+hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void* data_host, uint8_t* syn_host,
+                                   unsigned long long* corrected_host, void* workspace_dev,
+                                   uint64_t chunk, int n_streams) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_decode_host: m must be in [2, 6]");
+  if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_decode_host: size overflows");
+  if (corrected_host == nullptr || workspace_dev == nullptr)
+    return set_err(HAMMING_E_NULL, "hamming_decode_host: corrected or workspace is NULL");
+  if (N > 0 && (rx_host == nullptr || data_host == nullptr))
+    return set_err(HAMMING_E_NULL, "hamming_decode_host: rx or data is NULL");
+  if (n_streams < 1 || n_streams > 4 || chunk == 0 || chunk % kTileCw != 0)
+    return set_err(HAMMING_E_ARG, "hamming_decode_host: need 1 <= n_streams <= 4, chunk a multiple of 1024");
+  if (!aligned16(workspace_dev)) return set_err(HAMMING_E_MISALIGNED, "hamming_decode_host: workspace misaligned");
+  const uint64_t n = (1ull << m) - 1, k = n - m;
+  const HostSlotLayout L = host_slot_layout(m, chunk, syn_host != nullptr);
+  uint8_t* ws = static_cast<uint8_t*>(workspace_dev);
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(ws);
+  cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ready = nullptr;
+  hamming_status rc = HAMMING_OK;
+  cudaError_t e = cudaSuccess;
+  int launches = 0;
+  for (int i = 0; i < n_streams && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemsetAsync(total, 0, sizeof(unsigned long long), streams[0]);
+  if (e == cudaSuccess) e = cudaEventRecord(ready, streams[0]);
+  for (int i = 1; i < n_streams && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(streams[i], ready, 0);
+  if (e != cudaSuccess) rc = cuda_fail(e, "hamming_decode_host setup");
+  const uint8_t* hin = static_cast<const uint8_t*>(rx_host);
+  uint8_t* hout = static_cast<uint8_t*>(data_host);
+  for (uint64_t c0 = 0, i = 0; rc == HAMMING_OK && c0 < N; c0 += chunk, ++i) {
+    const uint64_t cn = std::min<uint64_t>(chunk, N - c0);
+    const int sl = static_cast<int>(i % n_streams);
+    cudaStream_t s = streams[sl];
+    uint8_t* d_rx = ws + 256 + sl * L.slot;
+    uint8_t* d_data = d_rx + L.rx;
+    uint8_t* d_syn = syn_host ? d_data + L.data : nullptr;
+    const uint64_t ib = (n * cn + 7) / 8, ob = (k * cn + 7) / 8;
+    e = cudaMemcpyAsync(d_rx, hin + c0 * n / 8, ib, cudaMemcpyHostToDevice, s);  // PS
+    if (e != cudaSuccess) { rc = cuda_fail(e, "hamming_decode_host H2D"); break; }
+    rc = decode_dispatch(m, d_rx, cn, d_data, d_syn, total, s, true);                   // DKE
+    if (rc != HAMMING_OK) break;
+    launches += g_launches;
+    e = cudaMemcpyAsync(hout + c0 * k / 8, d_data, ob, cudaMemcpyDeviceToHost, s);      // PR
+    if (e == cudaSuccess && syn_host) e = cudaMemcpyAsync(syn_host + c0, d_syn, cn, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "hamming_decode_host D2H"); break; }
+  }
+  for (int i = 0; i < n_streams; ++i) {
+    if (streams[i]) {
+      const cudaError_t e2 = cudaStreamSynchronize(streams[i]);
+      if (e2 != cudaSuccess && rc == HAMMING_OK) rc = cuda_fail(e2, "hamming_decode_host sync");
+    }
+  }
+  if (rc == HAMMING_OK) {
+    e = cudaMemcpy(corrected_host, total, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "hamming_decode_host count D2H");
+  }
+  if (ready) cudaEventDestroy(ready);
+  for (int i = 0; i < n_streams; ++i)
+    if (streams[i]) cudaStreamDestroy(streams[i]);
+  g_launches = launches;
+  return rc;
+}
+
+}  // extern "C"

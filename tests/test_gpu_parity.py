@@ -1,0 +1,171 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle,
+bit for bit, on identical seeded packets -- data stream, syndromes and the
+corrected count -- including multi-error codewords (where both must make the
+same miscorrection), ragged tails, empty input and every received word of
+the (7,4) and (15,11) codes."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1412_6862_b200 as ham
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [1, 31, 32, 33, 127, 128, 129, 1023, 1024, 1025, 4681, 3 * 1024 + 17, 7 * 1024, 50_000]
+
+
+def gpu(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_decode(m, rx_np, N, syndromes=True):
+    res = ham.decode(m, gpu(rx_np), N, syndromes=syndromes)
+    torch.cuda.synchronize()
+    data = res.data.cpu().numpy()[: ham.data_bytes(m, N)]
+    syn = res.syndromes.cpu().numpy()[:N] if res.syndromes is not None else None
+    return data, syn, int(res.corrected.item())
+
+
+def assert_same(m, N, got, want):
+    d, s, c = got
+    wd, ws, wc = want
+    assert d.shape == wd.shape
+    if not np.array_equal(d, wd):
+        bad = np.nonzero(d != wd)[0][:8]
+        raise AssertionError(f"m={m} N={N}: data differs at bytes {bad.tolist()}")
+    if s is not None:
+        if not np.array_equal(s, ws):
+            bad = np.nonzero(s != ws)[0][:8]
+            raise AssertionError(f"m={m} N={N}: syndromes differ at {bad.tolist()}: {s[bad]} vs {ws[bad]}")
+    assert c == wc, (m, N, c, wc)
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("N", SIZES)
+def test_decode_matches_oracle(oracle, m, N):
+    rx, _, _ = oracle.generate(m, 0x1412 + N, 0, N, p=0.5, q2=0.3)
+    assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+@pytest.mark.parametrize("m", [3, 6])
+def test_decode_without_syndromes(oracle, m):
+    N = 5000
+    rx, _, _ = oracle.generate(m, 5, 0, N, p=0.2, q2=0.5)
+    d, s, c = gpu_decode(m, rx, N, syndromes=False)
+    wd, _, wc = oracle.decode(m, rx, N)
+    assert s is None and np.array_equal(d, wd) and c == wc
+
+
+@pytest.mark.parametrize("m,N", [(2, 8), (3, 128), (4, 32768)])
+def test_every_received_word(oracle, m, N):
+    """All 2^n received words of the code, one codeword each."""
+    n = 2 ** m - 1
+    words = np.arange(N, dtype=np.int64)
+    bits = ((words[:, None] >> np.arange(n)) & 1).astype(np.uint8).reshape(-1)
+    rx = np.packbits(bits, bitorder="little")
+    assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+@pytest.mark.parametrize("m", [3, 5, 6])
+def test_uniform_random_streams_and_pad_bits(oracle, m):
+    """Uniformly random received bits (every codeword erroneous with high
+    probability) and garbage in the input pad bits, which must be ignored."""
+    rng = np.random.default_rng(m)
+    for N in (1, 1000, 1024 + 5, 20_003):
+        rx = rng.integers(0, 256, ham.coded_bytes(m, N), dtype=np.uint8)
+        assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+def test_channel_corners(oracle, m):
+    """p = 0 (nothing to correct), p = 1 single flips (paper regime: every
+    error corrected), p = 1 with q2 = 1 (every codeword miscorrected)."""
+    N = 3 * 1024 + 100
+    for p, q2 in ((0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (1e-3, 0.25)):
+        rx, sent, err = oracle.generate(m, 77, 0, N, p=p, q2=q2, want_sent=True, want_err=True)
+        got = gpu_decode(m, rx, N)
+        want = oracle.decode(m, rx, N)
+        assert_same(m, N, got, want)
+        e = err.reshape(N, 2)
+        if q2 == 0.0:
+            assert np.array_equal(got[0], sent) and got[2] == int((e[:, 0] > 0).sum())
+        if p == 1.0 and q2 == 1.0:
+            assert got[2] == N
+
+
+def test_empty_input_writes_zero_count():
+    cnt = torch.full((1,), 12345, dtype=torch.int64, device="cuda")
+    rx = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    data = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    ham.decode(6, rx, 0, data_out=data, syndromes=False, corrected=cnt)
+    torch.cuda.synchronize()
+    assert cnt.item() == 0
+
+
+@pytest.mark.parametrize("m", [3, 6])
+def test_canaries_past_the_end_untouched(oracle, m):
+    N = 2 * 1024 + 77
+    rx, _, _ = oracle.generate(m, 9, 0, N, p=0.3, q2=0.3)
+    db, sb = ham.data_bytes(m, N), N
+    data = torch.full((db + 64,), 0xA5, dtype=torch.uint8, device="cuda")
+    syn = torch.full((sb + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+    rx_t = torch.full((rx.size + 64,), 0xFF, dtype=torch.uint8, device="cuda")
+    rx_t[: rx.size] = gpu(rx)
+    res = ham.decode(m, rx_t, N, data_out=data, syndromes=syn)
+    torch.cuda.synchronize()
+    d = data.cpu().numpy()
+    s = syn.cpu().numpy()
+    assert (d[db:] == 0xA5).all() and (s[sb:] == 0x5A).all()
+    wd, ws, wc = oracle.decode(m, rx, N)
+    assert np.array_equal(d[:db], wd) and np.array_equal(s[:sb], ws) and res.corrected.item() == wc
+
+
+def test_repeated_calls_overwrite_count_and_are_deterministic(oracle):
+    m, N = 5, 40_000
+    rx, _, _ = oracle.generate(m, 3, 0, N, p=0.4, q2=0.2)
+    a = gpu_decode(m, rx, N)
+    b = gpu_decode(m, rx, N)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6])
+def test_gpu_generator_matches_oracle_generator(oracle, m):
+    """The GPU channel generator and the oracle's (written independently)
+    produce byte-identical packets; any range regenerates on its own."""
+    for c_first, N, p, q2 in ((0, 4681, 0.1, 0.0), (8 * 1000, 3 * 1024 + 9, 0.5, 0.5), (0, 2048, 1.0, 1.0),
+                              (123456, 1500, 0.0, 0.0)):
+        want, _, _ = oracle.generate(m, 0xBEEF, c_first, N, p=p, q2=q2)
+        got = ham.channel_generate(m, 0xBEEF, c_first, N, p=p, q2=q2)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy()[: want.size], want), (m, c_first, N, p, q2)
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6])
+def test_gpu_encoder_matches_oracle(oracle, m):
+    n, k = oracle.code_nk(m)
+    rng = np.random.default_rng(m)
+    for N in (1, 100, 1024, 5000):
+        data = rng.integers(0, 256, ham.data_bytes(m, N), dtype=np.uint8)
+        want = oracle.encode(m, data, N)
+        got = ham.encode(m, gpu(data), N)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy()[: want.size], want), (m, N)
+        # round trip through the GPU decoder
+        d, s, c = gpu_decode(m, got.cpu().numpy()[: want.size], N)
+        full = np.unpackbits(data, bitorder="little")[: N * k]
+        assert np.array_equal(np.unpackbits(d, bitorder="little")[: N * k], full) and c == 0
+
+
+@pytest.mark.parametrize("m", [3, 6])
+def test_decode_host_pipeline_matches_oracle(oracle, m):
+    N = 9 * 1024 + 300
+    rx, _, _ = oracle.generate(m, 21, 0, N, p=0.3, q2=0.3)
+    want = oracle.decode(m, rx, N)
+    chunk = 2048
+    for streams in (1, 3):
+        ws = torch.empty(ham.host_workspace_bytes(m, chunk, streams, True), dtype=torch.uint8, device="cuda")
+        rx_h = torch.from_numpy(rx).pin_memory()
+        data_h = torch.zeros(ham.data_bytes(m, N), dtype=torch.uint8).pin_memory()
+        syn_h = torch.zeros(N, dtype=torch.uint8).pin_memory()
+        cnt = ham.decode_host(m, rx_h, N, data_h, syn_h, ws, chunk_codewords=chunk, n_streams=streams)
+        assert_same(m, N, (data_h.numpy(), syn_h.numpy(), cnt), want)
