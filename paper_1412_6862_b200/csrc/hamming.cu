@@ -235,7 +235,7 @@ __device__ __forceinline__ void put_codeword(uint32_t (&o)[NO], int b, uint32_t 
 // ------------------------------------------------------------ tile operators
 // Each operator processes the 32 codewords of one lane: `in` = the lane's
 // IN_W input words, `out` = its OUT_W output words (both in shared memory),
-// `side` = 8 words of per-codeword bytes (syndromes), returns a count.
+// `side` = 8 words of per-codeword bytes (syndromes).
 // `valid` = number of the lane's 32 codewords that exist (32 except in the tail).
 
 template <int M>
@@ -246,7 +246,7 @@ struct DecodeOp {
   static constexpr bool HAS_SIDE = true;
   struct Args {};
 
-  __device__ __forceinline__ static uint32_t lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                   uint32_t (&side)[8], uint64_t /*cw0*/, int /*valid*/,
                                                   const Args&) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
@@ -256,7 +256,6 @@ struct DecodeOp {
     uint32_t o[k];
 #pragma unroll
     for (int i = 0; i < k; ++i) o[i] = 0;
-    uint32_t cnt = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       uint32_t lo, hi = 0;
@@ -276,11 +275,9 @@ struct DecodeOp {
         put_bits(o, c * k + 26, dhi, 31);
       }
       side[c >> 2] |= s << (8 * (c & 3));
-      cnt += (s != 0);
     }
 #pragma unroll
     for (int i = 0; i < k; ++i) out[i] = o[i];
-    return cnt;
   }
 };
 
@@ -292,7 +289,7 @@ struct EncodeOp {
   static constexpr bool HAS_SIDE = false;
   struct Args {};
 
-  __device__ __forceinline__ static uint32_t lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                   uint32_t (&)[8], uint64_t, int, const Args&) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     uint32_t w[k];
@@ -317,7 +314,6 @@ struct EncodeOp {
     }
 #pragma unroll
     for (int i = 0; i < n; ++i) out[i] = o[i];
-    return 0;
   }
 };
 
@@ -340,7 +336,7 @@ struct GenerateOp {
     int all;
   };
 
-  __device__ __forceinline__ static uint32_t lane(const uint32_t*, uint32_t* __restrict__ out, uint32_t (&)[8],
+  __device__ __forceinline__ static void lane(const uint32_t*, uint32_t* __restrict__ out, uint32_t (&)[8],
                                                   uint64_t cw0, int valid, const Args& a) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
@@ -381,7 +377,6 @@ struct GenerateOp {
     }
 #pragma unroll
     for (int i = 0; i < n; ++i) out[i] = o[i];
-    return 0;
   }
 };
 // ------------------------------------------------------------------ kernels
@@ -391,12 +386,80 @@ struct TileBytes {
   static constexpr int OUT = Op::OUT_W * 128;
 };
 
-// Persistent warp-tile pipeline: each warp owns STAGES input buffers (TMA bulk
-// loads, mbarrier-tracked) and 2 output buffers (TMA bulk stores).
+// Count of nonzero syndrome bytes in the lane's 8 side words (s <= 63, so
+// adding 0x7F to a byte never carries into the next one).
+__device__ __forceinline__ uint32_t count_nonzero_bytes(const uint32_t (&w)[8]) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += ((w[i] + 0x7F7F7F7Fu) & 0x80808080u) >> 7;
+  return (acc * 0x01010101u) >> 24;  // four byte lanes of at most 8 each
+}
+
+// The ragged last tile (rem < 1024 codewords) of a launch: bounded 16-byte
+// loads with zero fill, input pad bits past rem codewords cleared, the same
+// lane function, bounded stores.  Runs in the warp that owns the tile.
+template <class Op>
+__device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                               uint8_t* __restrict__ side, uint64_t tile, uint32_t rem,
+                                               uint64_t in_total, uint64_t out_total, uint8_t* ibuf,
+                                               uint32_t* obuf, int lane, const typename Op::Args& args) {
+  constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
+  if constexpr (IN > 0) {
+    const uint64_t ib0 = tile * IN;
+    const uint64_t nb = in_total - ib0;  // bytes of this tile that exist (< IN)
+    for (int i = lane * 16; i < IN; i += 512) {
+      if (static_cast<uint64_t>(i) + 16 <= nb) {
+        *reinterpret_cast<uint4*>(ibuf + i) = *reinterpret_cast<const uint4*>(in + ib0 + i);
+      } else {
+        for (int b = 0; b < 16; ++b) ibuf[i + b] = (static_cast<uint64_t>(i + b) < nb) ? in[ib0 + i + b] : 0;
+      }
+    }
+    __syncwarp();
+    const uint64_t vbits = static_cast<uint64_t>(rem) * Op::IN_BITS;  // clear the input pad bits
+    uint32_t* iw = reinterpret_cast<uint32_t*>(ibuf);
+    for (int i = lane; i < IN / 4; i += 32) {
+      const uint64_t b = static_cast<uint64_t>(i) * 32;
+      if (b >= vbits) iw[i] = 0;
+      else if (b + 32 > vbits) iw[i] &= (1u << (vbits - b)) - 1u;
+    }
+    __syncwarp();
+  }
+  const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
+  uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  Op::lane(reinterpret_cast<const uint32_t*>(ibuf) + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew,
+           tile * kTileCw + lane * 32, valid, args);
+  __syncwarp();
+  const uint64_t ob0 = tile * OUT;
+  const uint64_t nbo = out_total - ob0;
+  const uint8_t* ob = reinterpret_cast<const uint8_t*>(obuf);
+  for (int i = lane * 16; static_cast<uint64_t>(i) < nbo; i += 512) {
+    if (static_cast<uint64_t>(i) + 16 <= nbo) {
+      *reinterpret_cast<uint4*>(out + ob0 + i) = *reinterpret_cast<const uint4*>(ob + i);
+    } else {
+      for (int b = 0; static_cast<uint64_t>(i + b) < nbo; ++b) out[ob0 + i + b] = ob[i + b];
+    }
+  }
+  uint32_t cnt = 0;
+  if constexpr (Op::HAS_SIDE) {
+    if (side != nullptr) {
+      uint8_t* sp = side + tile * kTileCw + lane * 32;
+      for (int c = 0; c < valid; ++c) sp[c] = static_cast<uint8_t>(sidew[c >> 2] >> (8 * (c & 3)));
+    }
+    cnt = count_nonzero_bytes(sidew);  // codewords past `valid` decode zeros: s = 0
+  }
+  return cnt;
+}
+
+// Persistent warp-tile pipeline, one launch per call: each warp owns STAGES
+// input buffers (TMA bulk loads, mbarrier-tracked) and 2 output buffers (TMA
+// bulk stores) and walks full tiles gw, gw + nw, ...; the warp next in line
+// after the last full tile also takes the ragged tail.  The corrected count
+// (zeroed on the stream by the launcher) is reduced warp -> CTA -> one atomic.
 template <class Op, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
-                 uint64_t n_tiles, unsigned long long* __restrict__ counter, typename Op::Args args) {
+                 uint64_t n_full, uint32_t rem, uint64_t in_total, uint64_t out_total,
+                 unsigned long long* __restrict__ counter, typename Op::Args args) {
   constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   constexpr int WARP_SMEM = STAGES * IN + 2 * OUT;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -418,7 +481,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) {
         const uint64_t t = gw + s * nw;
-        if (t < n_tiles) {
+        if (t < n_full) {
           mbar_arrive_expect_tx(&bars[s], IN);
           bulk_g2s(wbase + s * IN, in + t * IN, IN, &bars[s], pol);
         }
@@ -429,7 +492,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   uint32_t cnt = 0;
   uint32_t it = 0;
-  for (uint64_t t = gw; t < n_tiles; t += nw, ++it) {
+  for (uint64_t t = gw; t < n_full; t += nw, ++it) {
     const int st = static_cast<int>(it % STAGES);
     if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
     uint32_t* obuf = reinterpret_cast<uint32_t*>(wbase + STAGES * IN + (it & 1u) * OUT);
@@ -437,7 +500,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
     uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
-    cnt += Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args);
+    Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args);
     fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
     __syncwarp();
     if (lane == 0) {
@@ -445,7 +508,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       bulk_commit();
       if constexpr (IN > 0) {
         const uint64_t nt = t + STAGES * nw;
-        if (nt < n_tiles) {
+        if (nt < n_full) {
           mbar_arrive_expect_tx(&bars[st], IN);
           bulk_g2s(wbase + st * IN, in + nt * IN, IN, &bars[st], pol);
         }
@@ -457,7 +520,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         st_global_cs_v4(sp, sidew[0], sidew[1], sidew[2], sidew[3]);
         st_global_cs_v4(sp + 16, sidew[4], sidew[5], sidew[6], sidew[7]);
       }
+      cnt += count_nonzero_bytes(sidew);
     }
+  }
+  if (rem > 0 && gw == n_full % nw) {  // the ragged tail tile
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+    cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
+                             reinterpret_cast<uint32_t*>(wbase + STAGES * IN), lane, args);
   }
   if (lane == 0) bulk_wait<0>();
 
@@ -467,59 +537,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0 && cnt) atomicAdd(&block_cnt, static_cast<unsigned long long>(cnt));
     __syncthreads();
     if (threadIdx.x == 0 && block_cnt) atomicAdd(counter, block_cnt);
-  }
-}
-
-// Ragged tail (fewer than 1024 codewords, possibly 0) in one warp.  Writes
-// *counter = tail count (a store, not an add): launched first on the stream,
-// it is the "overwrite" half of the count contract.
-template <class Op>
-__global__ void __launch_bounds__(32)
-    tail_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
-                uint64_t c0, uint32_t rem, uint64_t in_total, uint64_t out_total,
-                unsigned long long* __restrict__ counter, int accumulate, typename Op::Args args) {
-  constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
-  __shared__ __align__(16) uint32_t ibuf[IN > 0 ? IN / 4 : 1];
-  __shared__ __align__(16) uint32_t obuf[OUT / 4];
-  const int lane = threadIdx.x;
-  uint32_t cnt = 0;
-  if (rem > 0) {
-    if constexpr (IN > 0) {
-      const uint64_t ib0 = c0 * Op::IN_BITS / 8;  // c0 % 1024 == 0: byte aligned
-      const uint64_t nb = in_total - ib0;
-      uint8_t* ib = reinterpret_cast<uint8_t*>(ibuf);
-      for (int i = lane; i < IN; i += 32) ib[i] = (i < nb) ? in[ib0 + i] : 0;
-      __syncwarp();
-      const uint64_t vbits = static_cast<uint64_t>(rem) * Op::IN_BITS;  // zero the input pad bits
-      for (int i = lane; i < IN / 4; i += 32) {
-        const uint64_t b = static_cast<uint64_t>(i) * 32;
-        if (b >= vbits) ibuf[i] = 0;
-        else if (b + 32 > vbits) ibuf[i] &= (1u << (vbits - b)) - 1u;
-      }
-      __syncwarp();
-    }
-    const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
-    uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cnt = Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, c0 + lane * 32, valid, args);
-    __syncwarp();
-    const uint64_t ob0 = c0 / kTileCw * OUT;  // c0 is a whole number of tiles
-    const uint64_t nb = out_total - ob0;
-    const uint8_t* ob = reinterpret_cast<const uint8_t*>(obuf);
-    for (int i = lane; i < nb && i < OUT; i += 32) out[ob0 + i] = ob[i];
-    if constexpr (Op::HAS_SIDE) {
-      if (side != nullptr) {
-        const uint8_t* sb = reinterpret_cast<const uint8_t*>(sidew);
-        for (int c = 0; c < valid; ++c) side[c0 + lane * 32 + c] = sb[c];
-      }
-    }
-  }
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if (lane == 0 && counter != nullptr) {
-    if (accumulate) {
-      if (cnt) atomicAdd(counter, static_cast<unsigned long long>(cnt));
-    } else {
-      *counter = cnt;
-    }
   }
 }
 
@@ -576,23 +593,19 @@ struct Launcher {
       }
     }
     const int bps = (dev >= 0 && dev < kMaxDev) ? blocks_per_sm[dev].load(std::memory_order_relaxed) : 1;
-    const uint64_t n_tiles = n_cw / kTileCw;
-    const uint64_t c0 = n_tiles * kTileCw;
-    const uint32_t rem = static_cast<uint32_t>(n_cw - c0);
+    const uint64_t n_full = n_cw / kTileCw;
+    const uint32_t rem = static_cast<uint32_t>(n_cw - n_full * kTileCw);
     int launches = 0;
-    // tail first: it also initialises *counter
-    if (rem > 0 || (counter != nullptr && !accumulate)) {
-      tail_kernel<Op><<<1, 32, 0, stream>>>(in, out, side, c0, rem, in_total, out_total, counter,
-                                            accumulate ? 1 : 0, args);
-      ++launches;
-      e = cudaGetLastError();
-      if (e != cudaSuccess) return cuda_fail(e, "tail kernel launch");
+    if (counter != nullptr && !accumulate) {  // the count is overwritten, stream-ordered
+      e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
     }
     int grid = 0;
+    const uint64_t n_tiles = n_full + (rem > 0 ? 1 : 0);
     if (n_tiles > 0) {
       const uint64_t want = (n_tiles + WARPS - 1) / WARPS;
       grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * bps));
-      kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_tiles, counter, args);
+      kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_full, rem, in_total, out_total, counter, args);
       ++launches;
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e, "tiles kernel launch");

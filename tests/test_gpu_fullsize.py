@@ -44,7 +44,8 @@ def decode_config(oracle, m, N, seed, p, q2):
     torch.cuda.synchronize()
     check_windows(oracle, m, seed, N, p, q2, res)
     corrected = int(res.corrected.item())
-    nonzero = int(torch.count_nonzero(res.syndromes[:N]).item())
+    nonzero = sum(int(torch.count_nonzero(res.syndromes[i:min(N, i + (1 << 30))]).item())
+                  for i in range(0, N, 1 << 30))
     assert corrected == nonzero
     # every error event gives a nonzero syndrome (1 or 2 flips, p1 != p2)
     sd = np.sqrt(N * p * (1 - p)) if 0 < p < 1 else 0
