@@ -45,6 +45,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 
 #include "hamming.h"
 
@@ -244,11 +245,13 @@ struct DecodeOp {
   static constexpr int OUT_W = Geo<M>::k;
   static constexpr int IN_BITS = Geo<M>::n;  // per codeword
   static constexpr bool HAS_SIDE = true;
+  static constexpr int SHARED = 0;  // CTA-shared bytes (lookup tables)
   struct Args {};
+  __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                   uint32_t (&side)[8], uint64_t /*cw0*/, int /*valid*/,
-                                                  const Args&) {
+                                                  const Args&, const uint8_t* /*sh*/) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     uint32_t w[n];
 #pragma unroll
@@ -281,16 +284,126 @@ struct DecodeOp {
   }
 };
 
+// ----------------------------------------------------- lookup-table decoders
+// For m = 3 and 4 the POPC-per-index-set syndrome is bound by the XU pipe
+// (16 lanes/clk/SM) long before HBM is; a shared-memory
+// table turns the whole per-codeword decode (a2..a4) into one LDS on the
+// otherwise idle LSU pipe.  The table entries are produced by decode_cw<M>
+// itself, so the table IS the POPC decoder, evaluated once per index.
+
+// Lane-stream bits starting at b, placed at bit `at` of the result (bits below
+// `at` hold the preceding stream bits).  b and at are constants after unrolling.
+template <int NW>
+__device__ __forceinline__ uint32_t field_at(const uint32_t (&w)[NW], int b, int at) {
+  return (b >= at) ? take_bits(w, b - at) : (w[0] << (at - b));
+}
+
+// PRMT selectors that move byte 1 of the second operand into byte i of the first.
+__device__ __forceinline__ uint32_t insert_byte1(uint32_t word, uint32_t e, int i) {
+  const uint32_t sel = (i == 0) ? 0x3215u : (i == 1) ? 0x3250u : (i == 2) ? 0x3510u : 0x5210u;
+  return __byte_perm(word, e, sel);
+}
+
+// (7,4): per-lane replicated 128-entry table, entry = data (bits 0..3) |
+// syndrome << 8; lane l reads word [x][l], always its own bank (16 KB).
+struct DecodeLut3Op {
+  static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr int SHARED = 128 * 32 * 4;
+  struct Args {};
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    uint32_t* L = reinterpret_cast<uint32_t*>(sh);
+    for (int e = tid; e < 128 * 32; e += nth) {
+      uint32_t dlo, dhi;
+      const uint32_t s = decode_cw<3>(static_cast<uint32_t>(e >> 5) << 1, 0u, dlo, dhi);
+      L[e] = dlo | (s << 8);
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = in[i];
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t off = (field_at(w, 7 * c, 7) & 0x3F80u) | lane4;  // (x * 32 + lane) * 4
+      const uint32_t e = *reinterpret_cast<const uint32_t*>(sh + off);
+      const int r = (4 * c) & 31;
+      o[c >> 3] |= (e << r) & (0xFu << r);
+      side[c >> 2] = insert_byte1(side[c >> 2], e, c & 3);
+    }
+    *reinterpret_cast<uint4*>(out) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+};
+
+// (15,11): one 32768-entry table of 16-bit entries (64 KB, shared by the CTA),
+// entry = corrected data (bits 0..10) | syndrome << 12.  Built once per device
+// in global memory, copied into shared memory at CTA start.
+__device__ __align__(16) uint16_t g_lut15[32768];
+
+__global__ void init_lut15_kernel() {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < 32768) {
+    uint32_t dlo, dhi;
+    const uint32_t s = decode_cw<4>(static_cast<uint32_t>(x) << 1, 0u, dlo, dhi);
+    g_lut15[x] = static_cast<uint16_t>(dlo | (s << 12));
+  }
+}
+
+struct DecodeLut4Op {
+  static constexpr int IN_W = 15, OUT_W = 11, IN_BITS = 15;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr int SHARED = 32768 * 2;
+  struct Args {};
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    const uint4* src = reinterpret_cast<const uint4*>(g_lut15);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    for (int i = tid; i < SHARED / 16; i += nth) dst[i] = src[i];
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) w[i] = in[i];
+    uint32_t o[11];
+#pragma unroll
+    for (int i = 0; i < 11; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t off = field_at(w, 15 * c, 1) & 0xFFFEu;  // x * 2
+      const uint32_t e = *reinterpret_cast<const uint16_t*>(sh + off);
+      const int b = 11 * c, q = b >> 5, r = b & 31;
+      o[q] |= (e << r) & (0x7FFu << r);
+      if (r > 21) o[q + 1] |= (e >> (32 - r)) & (0x7FFu >> (32 - r));
+      side[c >> 2] = insert_byte1(side[c >> 2], e, c & 3);  // byte 1 = d8..d10, 0, s
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) side[i] = (side[i] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+    for (int i = 0; i < 11; ++i) out[i] = o[i];
+  }
+};
+
 template <int M>
 struct EncodeOp {
   static constexpr int IN_W = Geo<M>::k;
   static constexpr int OUT_W = Geo<M>::n;
   static constexpr int IN_BITS = Geo<M>::k;
   static constexpr bool HAS_SIDE = false;
+  static constexpr int SHARED = 0;
   struct Args {};
+  __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                  uint32_t (&)[8], uint64_t, int, const Args&) {
+                                                  uint32_t (&)[8], uint64_t, int, const Args&, const uint8_t*) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     uint32_t w[k];
 #pragma unroll
@@ -331,13 +444,15 @@ struct GenerateOp {
   static constexpr int OUT_W = Geo<M>::n;
   static constexpr int IN_BITS = 0;
   static constexpr bool HAS_SIDE = false;
+  static constexpr int SHARED = 0;
   struct Args {
     uint64_t seed, c_first, thresh, q2thresh;
     int all;
   };
+  __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
 
   __device__ __forceinline__ static void lane(const uint32_t*, uint32_t* __restrict__ out, uint32_t (&)[8],
-                                                  uint64_t cw0, int valid, const Args& a) {
+                                                  uint64_t cw0, int valid, const Args& a, const uint8_t*) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
     uint32_t o[n];
@@ -402,7 +517,8 @@ template <class Op>
 __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
                                                uint8_t* __restrict__ side, uint64_t tile, uint32_t rem,
                                                uint64_t in_total, uint64_t out_total, uint8_t* ibuf,
-                                               uint32_t* obuf, int lane, const typename Op::Args& args) {
+                                               uint32_t* obuf, int lane, const typename Op::Args& args,
+                                               const uint8_t* sh) {
   constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   if constexpr (IN > 0) {
     const uint64_t ib0 = tile * IN;
@@ -427,7 +543,7 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
   const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
   uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   Op::lane(reinterpret_cast<const uint32_t*>(ibuf) + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew,
-           tile * kTileCw + lane * 32, valid, args);
+           tile * kTileCw + lane * 32, valid, args, sh);
   __syncwarp();
   const uint64_t ob0 = tile * OUT;
   const uint64_t nbo = out_total - ob0;
@@ -466,13 +582,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   __shared__ unsigned long long block_cnt;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* wbase = smem + warp * WARP_SMEM;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * WARP_SMEM) + warp * STAGES;
+  uint8_t* const sh = smem;  // Op::SHARED bytes of CTA-wide tables first
+  uint8_t* wbase = smem + Op::SHARED + warp * WARP_SMEM;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Op::SHARED + WARPS * WARP_SMEM) + warp * STAGES;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
 
   if (threadIdx.x == 0) block_cnt = 0;
+  if constexpr (Op::SHARED > 0) {
+    Op::cta_init(sh, threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
   if constexpr (IN > 0) {
     if (lane == 0) {
 #pragma unroll
@@ -500,7 +621,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
     uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
-    Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args);
+    Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args, sh);
     fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
     __syncwarp();
     if (lane == 0) {
@@ -527,7 +648,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
     cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
-                             reinterpret_cast<uint32_t*>(wbase + STAGES * IN), lane, args);
+                             reinterpret_cast<uint32_t*>(wbase + STAGES * IN), lane, args, sh);
   }
   if (lane == 0) bulk_wait<0>();
 
@@ -569,7 +690,8 @@ int sm_count(int dev) {
 template <class Op, int WARPS, int STAGES>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
-  static constexpr size_t SMEM = static_cast<size_t>(WARPS) * (STAGES * IN + 2 * OUT) + WARPS * STAGES * 8;
+  static constexpr size_t SMEM =
+      Op::SHARED + static_cast<size_t>(WARPS) * (STAGES * IN + 2 * OUT) + WARPS * STAGES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
   static hamming_status run(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t n_cw, uint64_t in_total,
@@ -636,21 +758,48 @@ bool bits_overflow(int m, uint64_t N) {
   return N > (~0ull) / n;
 }
 
+// One-time per-device build of the (15,11) table in global memory.
+std::once_flag g_lut15_once[kMaxDev];
+cudaError_t g_lut15_err[kMaxDev];
+
+hamming_status ensure_lut15(int dev) {
+  if (dev < 0 || dev >= kMaxDev) return set_err(HAMMING_E_CUDA, "device index out of range");
+  std::call_once(g_lut15_once[dev], [dev] {
+    cudaStream_t s = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+      init_lut15_kernel<<<32768 / 256, 256, 0, s>>>();
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    g_lut15_err[dev] = e;
+  });
+  if (g_lut15_err[dev] != cudaSuccess) return cuda_fail(g_lut15_err[dev], "building the (15,11) table");
+  return HAMMING_OK;
+}
+
 hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
                                unsigned long long* counter, cudaStream_t st, bool accumulate) {
   const uint64_t n = (1ull << m) - 1, k = n - m;
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
   switch (m) {
-#define HAMMING_DECODE_CASE(MM)                                                                          \
-  case MM:                                                                                               \
-    return Launcher<DecodeOp<MM>, Shape<MM>::W, Shape<MM>::S>::run(in, out, syn, N, ib, ob, counter, {}, \
-                                                                   st, accumulate);
-    HAMMING_DECODE_CASE(2)
-    HAMMING_DECODE_CASE(3)
-    HAMMING_DECODE_CASE(4)
-    HAMMING_DECODE_CASE(5)
-    HAMMING_DECODE_CASE(6)
-#undef HAMMING_DECODE_CASE
+    case 2:
+      return Launcher<DecodeOp<2>, 16, 4>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+    case 3:
+      return Launcher<DecodeLut3Op, 16, 6>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+    case 4: {
+      int dev = 0;
+      const cudaError_t e = cudaGetDevice(&dev);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+      const hamming_status rc = ensure_lut15(dev);
+      if (rc != HAMMING_OK) return rc;
+      return Launcher<DecodeLut4Op, 12, 4>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+    }
+    case 5:
+      return Launcher<DecodeOp<5>, 12, 3>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+    case 6:
+      return Launcher<DecodeOp<6>, 7, 2>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
   }
   return set_err(HAMMING_E_INVALID_M, "decode: m must be in [2, 6]");
 }
