@@ -78,7 +78,7 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
-        q = "clocks.sm,clocks.max.sm," + ",".join(REASON_FIELDS)
+        q = "clocks.sm,clocks.max.sm," + ",".join(REASON_FIELDS) + ",clocks.mem,power.draw"
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -93,7 +93,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 2 + len(REASON_FIELDS):
+            if len(parts) >= 4 + len(REASON_FIELDS):
                 self.rows.append(parts)
 
     def stop(self):
@@ -114,9 +114,15 @@ class ClockSampler:
             for name, val in zip(REASON_FIELDS, r[2:]):
                 if val.lower() == "active":
                     reasons.add(name.split(".")[-1])
+
+        def med(col):
+            v = sorted(float(r[col]) for r in self.rows if r[col].replace(".", "").isdigit())
+            return v[len(v) // 2] if v else None
+
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "mem_mhz": med(2 + len(REASON_FIELDS)), "power_w": med(3 + len(REASON_FIELDS))}
 
 
 # ------------------------------------------------------------- cpu baseline
@@ -298,9 +304,12 @@ def main():
         try:
             with open(prof) as f:
                 pj = json.load(f)
-            key = f"m{m}_{'syn' if syn is not None else 'nosyn'}"
-            if key in pj:
-                traffic = round(pj[key]["traffic_per_alg_byte"] * alg_bytes)
+            for v in pj.values():
+                if v["m"] == m and v["syndromes"] == (syn is not None):
+                    if v["n_codewords"] == n_loc:   # the very launch bench times
+                        traffic = int(v["traffic"])
+                    else:                            # same kernel, other size: per algorithmic byte
+                        traffic = round(v["traffic_per_alg_byte"] * alg_bytes)
         except Exception:
             traffic = None
 
@@ -317,7 +326,7 @@ def main():
                    "l2": "inputs larger than L2 (no flush needed)", "grid_blocks": grid},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": f"tiles_kernel<DecodeOp<{m}>> (+1 tail warp) per hamming_decode call",
+                     "kernel": f"tiles_kernel decode m={m} (one launch + 8-byte memset per hamming_decode call)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(k_ms, 4), "peak_source": peak_src},
         "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,

@@ -10,7 +10,9 @@ import os
 import re
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhamming.so")
+# HAMMING_LIB points the binding at another build of the same source (launch-shape
+# tuning sweeps, tools/tune_shapes.sh); the default is the in-tree library.
+LIB_PATH = os.environ.get("HAMMING_LIB") or os.path.join(_PKG, "libhamming.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "hamming.h")
 
 STATUS = {

@@ -36,20 +36,28 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in (SRC, HDR))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if out == LIB and not force and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, "-cudart", "static", *[f"-D{d}" for d in defines],
+           "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libhamming.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-o", default=LIB)
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.o, defines=a.D))

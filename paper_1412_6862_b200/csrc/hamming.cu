@@ -256,6 +256,7 @@ struct DecodeOp {
     uint32_t w[n];
 #pragma unroll
     for (int i = 0; i < n; ++i) w[i] = in[i];
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     uint32_t o[k];
 #pragma unroll
     for (int i = 0; i < k; ++i) o[i] = 0;
@@ -327,6 +328,7 @@ struct DecodeLut3Op {
     uint32_t w[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) w[i] = in[i];
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     const uint32_t lane4 = (threadIdx.x & 31u) << 2;
     uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -373,6 +375,7 @@ struct DecodeLut4Op {
     uint32_t w[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) w[i] = in[i];
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     uint32_t o[11];
 #pragma unroll
     for (int i = 0; i < 11; ++i) o[i] = 0;
@@ -567,17 +570,30 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
 }
 
 // Persistent warp-tile pipeline, one launch per call: each warp owns STAGES
-// input buffers (TMA bulk loads, mbarrier-tracked) and 2 output buffers (TMA
-// bulk stores) and walks full tiles gw, gw + nw, ...; the warp next in line
-// after the last full tile also takes the ragged tail.  The corrected count
-// (zeroed on the stream by the launcher) is reduced warp -> CTA -> one atomic.
-template <class Op, int WARPS, int STAGES>
+// tile buffers filled by TMA bulk loads (mbarrier-tracked) and walks full tiles
+// gw, gw + nw, ...; the warp next in line after the last full tile also takes
+// the ragged tail.  Decoders write their (smaller) output tile IN PLACE over
+// the consumed input tile and bulk-store it from there; the stage is refilled
+// at the next iteration, once that store has read it.  Ops whose output is
+// larger than the input (encode, generate) use two separate output buffers.
+// The corrected count (zeroed on the stream by the launcher) is reduced
+// warp -> CTA -> one atomic.
+template <class Op, bool WANT_IN_PLACE = true>
+struct TileLayout {
+  static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
+  static constexpr bool IN_PLACE = WANT_IN_PLACE && IN > 0 && OUT <= IN;
+  static constexpr int OUT_BUFS = IN_PLACE ? 0 : 2;
+  __host__ __device__ static constexpr int warp_bytes(int stages) { return stages * IN + OUT_BUFS * OUT; }
+};
+
+template <class Op, int WARPS, int STAGES, bool INPLACE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
                  uint64_t n_full, uint32_t rem, uint64_t in_total, uint64_t out_total,
                  unsigned long long* __restrict__ counter, typename Op::Args args) {
-  constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
-  constexpr int WARP_SMEM = STAGES * IN + 2 * OUT;
+  using TL = TileLayout<Op, INPLACE>;
+  constexpr int IN = TL::IN, OUT = TL::OUT;
+  constexpr int WARP_SMEM = TL::warp_bytes(STAGES);
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long block_cnt;
 
@@ -615,10 +631,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   uint32_t it = 0;
   for (uint64_t t = gw; t < n_full; t += nw, ++it) {
     const int st = static_cast<int>(it % STAGES);
-    if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
-    uint32_t* obuf = reinterpret_cast<uint32_t*>(wbase + STAGES * IN + (it & 1u) * OUT);
-    if (lane == 0) bulk_wait_read<1>();  // the store issued two tiles ago has read obuf
-    __syncwarp();
+    uint32_t* obuf;
+    if constexpr (TL::IN_PLACE) {
+      mbar_wait(&bars[st], (it / STAGES) & 1u);
+      obuf = reinterpret_cast<uint32_t*>(wbase + st * IN);
+    } else {
+      if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
+      obuf = reinterpret_cast<uint32_t*>(wbase + STAGES * IN + (it & 1u) * OUT);
+      if (lane == 0) bulk_wait_read<1>();  // the store issued two tiles ago has read obuf
+      __syncwarp();
+    }
     uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
     Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args, sh);
@@ -627,7 +649,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) {
       bulk_s2g(out + t * OUT, obuf, OUT, pol);
       bulk_commit();
-      if constexpr (IN > 0) {
+      if constexpr (TL::IN_PLACE) {
+        // refill the stage of the PREVIOUS tile: its in-place store was issued a
+        // whole tile ago, so waiting for it to have read shared memory is free
+        if (it > 0) {
+          const uint64_t nt = t - nw + STAGES * nw;
+          if (nt < n_full) {
+            const int ps = static_cast<int>((it - 1) % STAGES);
+            bulk_wait_read<1>();
+            mbar_arrive_expect_tx(&bars[ps], IN);
+            bulk_g2s(wbase + ps * IN, in + nt * IN, IN, &bars[ps], pol);
+          }
+        }
+      }
+      if constexpr (!TL::IN_PLACE && IN > 0) {
         const uint64_t nt = t + STAGES * nw;
         if (nt < n_full) {
           mbar_arrive_expect_tx(&bars[st], IN);
@@ -647,8 +682,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   if (rem > 0 && gw == n_full % nw) {  // the ragged tail tile
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    uint8_t* tail_out = TL::IN_PLACE ? wbase : wbase + STAGES * IN;
     cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
-                             reinterpret_cast<uint32_t*>(wbase + STAGES * IN), lane, args, sh);
+                             reinterpret_cast<uint32_t*>(tail_out), lane, args, sh);
   }
   if (lane == 0) bulk_wait<0>();
 
@@ -687,11 +723,11 @@ int sm_count(int dev) {
   return v;
 }
 
-template <class Op, int WARPS, int STAGES>
+template <class Op, int WARPS, int STAGES, bool INPLACE = true>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   static constexpr size_t SMEM =
-      Op::SHARED + static_cast<size_t>(WARPS) * (STAGES * IN + 2 * OUT) + WARPS * STAGES * 8;
+      Op::SHARED + static_cast<size_t>(WARPS) * TileLayout<Op, INPLACE>::warp_bytes(STAGES) + WARPS * STAGES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
   static hamming_status run(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t n_cw, uint64_t in_total,
@@ -702,7 +738,7 @@ struct Launcher {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    auto kfn = tiles_kernel<Op, WARPS, STAGES>;
+    auto kfn = tiles_kernel<Op, WARPS, STAGES, INPLACE>;
     if (dev < 0 || dev >= kMaxDev || !configured[dev].load(std::memory_order_acquire)) {
       e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -758,6 +794,54 @@ bool bits_overflow(int m, uint64_t N) {
   return N > (~0ull) / n;
 }
 
+// Decode launch shapes: warps per CTA, TMA stages per warp, output in place
+// (DESIGN.md section 5).  Overridable at build time for tuning sweeps only.
+#ifndef HAM_W2
+#define HAM_W2 16
+#endif
+#ifndef HAM_S2
+#define HAM_S2 8
+#endif
+#ifndef HAM_IP2
+#define HAM_IP2 true
+#endif
+#ifndef HAM_W3
+#define HAM_W3 16
+#endif
+#ifndef HAM_S3
+#define HAM_S3 12
+#endif
+#ifndef HAM_IP3
+#define HAM_IP3 true
+#endif
+#ifndef HAM_W4
+#define HAM_W4 8
+#endif
+#ifndef HAM_S4
+#define HAM_S4 8
+#endif
+#ifndef HAM_IP4
+#define HAM_IP4 true
+#endif
+#ifndef HAM_W5
+#define HAM_W5 12
+#endif
+#ifndef HAM_S5
+#define HAM_S5 3
+#endif
+#ifndef HAM_IP5
+#define HAM_IP5 false
+#endif
+#ifndef HAM_W6
+#define HAM_W6 8
+#endif
+#ifndef HAM_S6
+#define HAM_S6 3
+#endif
+#ifndef HAM_IP6
+#define HAM_IP6 true
+#endif
+
 // One-time per-device build of the (15,11) table in global memory.
 std::once_flag g_lut15_once[kMaxDev];
 cudaError_t g_lut15_err[kMaxDev];
@@ -785,21 +869,26 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
   switch (m) {
     case 2:
-      return Launcher<DecodeOp<2>, 16, 4>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      return Launcher<DecodeOp<2>, HAM_W2, HAM_S2, HAM_IP2>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                 accumulate);
     case 3:
-      return Launcher<DecodeLut3Op, 16, 6>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      return Launcher<DecodeLut3Op, HAM_W3, HAM_S3, HAM_IP3>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                  accumulate);
     case 4: {
       int dev = 0;
       const cudaError_t e = cudaGetDevice(&dev);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
       const hamming_status rc = ensure_lut15(dev);
       if (rc != HAMMING_OK) return rc;
-      return Launcher<DecodeLut4Op, 12, 4>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      return Launcher<DecodeLut4Op, HAM_W4, HAM_S4, HAM_IP4>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                  accumulate);
     }
     case 5:
-      return Launcher<DecodeOp<5>, 12, 3>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      return Launcher<DecodeOp<5>, HAM_W5, HAM_S5, HAM_IP5>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                 accumulate);
     case 6:
-      return Launcher<DecodeOp<6>, 7, 2>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      return Launcher<DecodeOp<6>, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                 accumulate);
   }
   return set_err(HAMMING_E_INVALID_M, "decode: m must be in [2, 6]");
 }

@@ -1,19 +1,43 @@
-import torch, time, sys
-sys.path.insert(0, '.')
-import paper_1412_6862_b200 as ham
-for m in (3,4,5,6):
-    n,k = ham.code_nk(m)
-    N = (1<<31)*8//n//1024*1024   # 2 GiB coded
+"""Quick device-timed decode throughput (min of 8 launches) for tuning.
+
+    python tools/quick_bench.py [--m 3 4 5 6] [--gib 2] [--reps 8]
+Not the benchmark of record (that is bench.py)."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1412_6862_b200 as ham  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--m", type=int, nargs="+", default=[3, 4, 5, 6])
+ap.add_argument("--gib", type=float, default=2.0)
+ap.add_argument("--reps", type=int, default=8)
+ap.add_argument("--tag", default="")
+a = ap.parse_args()
+peak = 6548.2
+for m in a.m:
+    n, k = ham.code_nk(m)
+    N = int(a.gib * (1 << 30) * 8) // n // 1024 * 1024
     rx = ham.channel_generate(m, 1, 0, N, p=0.1)
     res = ham.decode(m, rx, N)
     torch.cuda.synchronize()
     for syn in (True, False):
-        ts=[]
-        for i in range(8):
-            s=torch.cuda.Event(enable_timing=True); e=torch.cuda.Event(enable_timing=True)
-            s.record(); ham.decode(m, rx, N, data_out=res.data, syndromes=res.syndromes if syn else False, corrected=res.corrected); e.record(); torch.cuda.synchronize()
+        ts = []
+        for _ in range(a.reps):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            ham.decode(m, rx, N, data_out=res.data, syndromes=res.syndromes if syn else False,
+                       corrected=res.corrected)
+            e.record()
+            torch.cuda.synchronize()
             ts.append(s.elapsed_time(e))
-        t=min(ts)/1e3
-        by = ham.coded_bytes(m,N)+ham.data_bytes(m,N)+(N if syn else 0)
-        print(f"m={m} syn={syn} N={N} t={t*1e3:.3f}ms  {n*N/t/1e9:.0f} Gbit/s  {by/t/1e9:.0f} GB/s grid={ham.last_grid_blocks()}", flush=True)
-    del rx, res; torch.cuda.empty_cache()
+        t = min(ts) / 1e3
+        by = ham.coded_bytes(m, N) + ham.data_bytes(m, N) + (N if syn else 0)
+        print(f"{a.tag} m={m} syn={syn} N={N} t={t * 1e3:.3f}ms {n * N / t / 1e9:.0f} Gbit/s "
+              f"{by / t / 1e9:.0f} GB/s ({by / t / 1e9 / peak:.3f}) grid={ham.last_grid_blocks()}", flush=True)
+    del rx, res
+    torch.cuda.empty_cache()

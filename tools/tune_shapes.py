@@ -1,0 +1,53 @@
+"""Launch-shape sweep: `python tools/tune_shapes.py build` compiles variants of
+libhamming.so into build/tune/ (CPU box); `python tools/tune_shapes.py run`
+times each on the GPU via HAMMING_LIB + tools/quick_bench.py."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "tune")
+
+VARIANTS = {
+    # m: list of (W, S, in_place)
+    3: [(16, 8, 1), (16, 6, 0), (32, 4, 1), (16, 12, 1)],
+    4: [(16, 4, 1), (12, 4, 0), (16, 5, 1), (8, 8, 1)],
+    5: [(16, 3, 1), (12, 3, 0), (12, 4, 1), (8, 6, 1), (8, 4, 0), (16, 2, 1)],
+    6: [(8, 3, 1), (7, 2, 0), (4, 6, 1), (8, 2, 1), (4, 5, 1)],
+}
+
+
+def name(m, v):
+    return f"m{m}_w{v[0]}_s{v[1]}_ip{v[2]}"
+
+
+def build():
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1412_6862_b200 import build as b
+    os.makedirs(OUT, exist_ok=True)
+    for f in os.listdir(OUT):
+        os.remove(os.path.join(OUT, f))
+    jobs = []
+    for m, vs in VARIANTS.items():
+        for v in vs:
+            # the other m keep their defaults
+            defs = [f"HAM_W{m}={v[0]}", f"HAM_S{m}={v[1]}", f"HAM_IP{m}={'true' if v[2] else 'false'}"]
+            jobs.append((os.path.join(OUT, name(m, v) + ".so"), defs))
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
+        for path in ex.map(lambda j: b.build(force=True, out=j[0], defines=j[1]), jobs):
+            print("built", path, flush=True)
+
+
+def run():
+    for m, vs in VARIANTS.items():
+        for v in vs:
+            path = os.path.join(OUT, name(m, v) + ".so")
+            env = dict(os.environ, HAMMING_LIB=path)
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--m", str(m),
+                            "--tag", name(m, v)], env=env)
+
+
+if __name__ == "__main__":
+    {"build": build, "run": run}[sys.argv[1]]()
