@@ -156,6 +156,18 @@ __device__ __forceinline__ void put_bits(uint32_t (&o)[NO], int b, uint32_t val,
   if (r != 0 && r + width > 32) o[q + 1] |= val >> (32 - r);
 }
 
+// OR bits [pos, pos+len) of src into the output stream at bit b: one shift and
+// one LOP3 per output word touched (all shifts are constants after unrolling).
+// Used to move each redundancy-removal group straight to its final position.
+template <int NO>
+__device__ __forceinline__ void put_field(uint32_t (&o)[NO], int b, uint32_t src, int pos, int len) {
+  const int q = b >> 5, r = b & 31;
+  const uint32_t m = (len >= 32) ? 0xFFFFFFFFu : ((1u << len) - 1u);
+  const uint32_t x = (r >= pos) ? (src << (r - pos)) : (src >> (pos - r));
+  o[q] |= x & (m << r);
+  if (r + len > 32) o[q + 1] |= (src >> (pos + 32 - r)) & (m >> (32 - r));
+}
+
 // --------------------------------------------------------- per-codeword math
 // Decode one codeword given as v = (lo, hi): bit p of v holds position p
 // (hi bit i = position 32 + i; hi unused for m <= 5).  Returns the syndrome s
@@ -188,6 +200,23 @@ __device__ __forceinline__ uint32_t decode_cw(uint32_t lo, uint32_t hi, uint32_t
     for (int g = 1; g < 5; ++g) d |= (lo >> (g + 2)) & dmask(g);
     dlo = d;        // data bits 0..25 (positions 3..31)
     dhi = hi >> 1;  // data bits 26..56 (positions 33..63)
+  }
+  return s;
+}
+
+// The syndrome alone (a2): s = sum_j 2^j parity(v & M_j), folded for m = 6.
+template <int M>
+__device__ __forceinline__ uint32_t syndrome_cw(uint32_t lo, uint32_t hi) {
+  constexpr int n = Geo<M>::n;
+  uint32_t s = 0;
+  if constexpr (M <= 5) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) s |= static_cast<uint32_t>(__popc(lo & pmask(n, j)) & 1) << j;
+  } else {
+    const uint32_t x = lo ^ hi;
+    s = static_cast<uint32_t>(__popc(hi) & 1) << 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) s |= static_cast<uint32_t>(__popc(x & pmask(31, j)) & 1) << j;
   }
   return s;
 }
@@ -270,14 +299,20 @@ struct DecodeOp {
         lo = take_bits(w, c * n - 1);
         if constexpr (M == 6) hi = take_bits(w, c * n + 31);
       }
-      uint32_t dlo, dhi;
-      const uint32_t s = decode_cw<M>(lo, hi, dlo, dhi);
-      if constexpr (M <= 5) {
-        put_bits(o, c * k, dlo, k);
+      const uint32_t s = syndrome_cw<M>(lo, hi);                    // a2
+      if constexpr (M <= 5) {                                       // a3
+        lo ^= 1u << s;
       } else {
-        put_bits(o, c * k, dlo, 26);
-        put_bits(o, c * k + 26, dhi, 31);
+        const uint64_t f = 1ull << s;
+        lo ^= static_cast<uint32_t>(f);
+        hi ^= static_cast<uint32_t>(f >> 32);
       }
+      // a4 + a5: each redundancy-removal group (positions 2^g+1 .. 2^(g+1)-1,
+      // data bits from 2^g-g-1) goes straight to its place in the output stream
+#pragma unroll
+      for (int g = 1; g < (M <= 5 ? M : 5); ++g)
+        put_field(o, c * k + (1 << g) - g - 1, lo, (1 << g) + 1, (1 << g) - 1);
+      if constexpr (M == 6) put_field(o, c * k + 26, hi, 1, 31);
       side[c >> 2] |= s << (8 * (c & 3));
     }
 #pragma unroll
