@@ -132,6 +132,48 @@ hamming_status hamming_decode_host(int m, const void *rx_host, uint64_t n_codewo
                                    void *workspace_dev, uint64_t chunk_codewords,
                                    int n_streams);
 
+/* ------------------------------------- packets: the paper's workload (f2) */
+
+/* The paper's packets (Fig. 1): a message of msg_bytes bytes
+ * (1..4096) is split into t segments (1..16) -- the first (8*msg_bytes mod t)
+ * get ceil(8*msg_bytes/t) message bits, the rest floor (DESIGN.md reading
+ * R14) -- and segment i is ONE shortened Hamming codeword of k_i message bits
+ * and the minimal r_i with 2^r >= k + r + 1, n_i = k_i + r_i.  The
+ * encoded packet is H_1 ... H_t concatenated bitwise, LSB-first.  Packet j
+ * starts at byte j*rx_stride (rx_stride a multiple of 16, >= the coded bytes
+ * rounded up to 16); its message at byte j*msg_stride. */
+uint64_t hamming_packet_coded_bytes(uint32_t msg_bytes, int t); /* 0 on bad arguments */
+hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t *seg_k_host, uint32_t *seg_n_host);
+
+/* hamming_decode_packets -- per segment: syndrome, ED/EC:
+ * s = 0 clean, 1 <= s <= n_i flip position s, s > n_i uncorrectable (the
+ * segment is left as received, reading R15); RR and merger.
+ *   syndromes_dev: n_packets*t uint16 or NULL; status_dev: n_packets bytes or
+ *   NULL (0 clean, 1 corrected, 2 some segment uncorrectable); counts_dev: 2
+ *   device uint64 or NULL, OVERWRITTEN with {segments corrected, segments
+ *   uncorrectable}.  rx 16-byte aligned; buffers must not overlap. */
+hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void *rx_dev, uint64_t rx_stride,
+                                      uint64_t n_packets, void *msg_dev, uint64_t msg_stride,
+                                      uint16_t *syndromes_dev, uint8_t *status_dev,
+                                      unsigned long long *counts_dev, void *stream);
+
+/* hamming_encode_packets -- the transmitter ("exact reverse process"):
+ * messages (msg_stride apart) -> packets (rx_stride apart, pad bits 0). */
+hamming_status hamming_encode_packets(uint32_t msg_bytes, int t, const void *msg_dev, uint64_t msg_stride,
+                                      uint64_t n_packets, void *rx_dev, uint64_t rx_stride, void *stream);
+
+/* hamming_packet_channel_generate -- seeded synthetic received packets (test
+ * and benchmark input, the oracle's oracle_generate_packets written
+ * independently): for global packet index g, key = mix(seed + (g+1) gamma),
+ * u(g,q) = mix(key + (q+1) gamma); message byte b = byte (b&7) of u(g, b>>3);
+ * W = ceil(msg_bytes/8); segment i gets one flip iff all or u(g, W+2i) < thresh,
+ * at position 1 + umulhi(lo32(u(g, W+2i+1)), n_i) -- one error per segment,
+ * the paper's t-error regime.  msg_dev (nullable) receives the sent messages,
+ * msg_bytes apart. */
+hamming_status hamming_packet_channel_generate(uint32_t msg_bytes, int t, uint64_t seed, uint64_t g_first,
+                                               uint64_t n_packets, uint64_t thresh, int all, void *rx_dev,
+                                               uint64_t rx_stride, void *msg_dev, void *stream);
+
 /* --------------------------------------------------------------- helpers */
 
 uint64_t hamming_coded_bytes(int m, uint64_t n_codewords); /* ceil(n*N/8), 0 on bad m */

@@ -59,6 +59,14 @@ def lib() -> ctypes.CDLL:
         L.oracle_encode.argtypes = [ctypes.c_int, ctypes.c_void_p, u64, ctypes.c_void_p]
         L.oracle_generate.argtypes = [ctypes.c_int, u64, u64, u64, u64, ctypes.c_int, u64,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.oracle_packet_layout.argtypes = [ctypes.c_uint32, ctypes.c_int, u32p, u32p]
+        L.oracle_packet_layout.restype = ctypes.c_long
+        L.oracle_encode_packet.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_decode_packet.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p]
+        L.oracle_generate_packets.argtypes = [ctypes.c_uint32, ctypes.c_int, u64, u64, u64, u64, ctypes.c_int,
+                                              ctypes.c_void_p, u64, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -223,3 +231,80 @@ def generate(m: int, seed: int, c_first: int, count: int, p: float = 0.1, q2: fl
     with ThreadPoolExecutor(max(1, threads)) as ex:
         list(ex.map(run, _ranges(count, threads)))
     return rx, sent, err
+
+
+# ------------------------------------------------ packets (the paper's workload)
+def packet_layout(msg_bits: int, t: int):
+    """(seg_k, seg_n, total coded bits) -- near-equal split, larger first."""
+    k = (ctypes.c_uint32 * max(1, t))()
+    n = (ctypes.c_uint32 * max(1, t))()
+    total = lib().oracle_packet_layout(msg_bits, t, k, n)
+    if total < 0:
+        raise ValueError(f"packet_layout: bad (msg_bits={msg_bits}, t={t})")
+    return list(k[:t]), list(n[:t]), int(total)
+
+
+def packet_coded_bytes(msg_bytes: int, t: int) -> int:
+    return (packet_layout(msg_bytes * 8, t)[2] + 7) // 8
+
+
+def encode_packet(msg_bytes: int, t: int, msg: np.ndarray) -> np.ndarray:
+    msg = np.ascontiguousarray(msg, dtype=np.uint8)
+    rx = np.zeros(packet_coded_bytes(msg_bytes, t), np.uint8)
+    if lib().oracle_encode_packet(msg_bytes, t, _ptr(msg), _ptr(rx)) != 0:
+        raise RuntimeError("oracle_encode_packet failed")
+    return rx
+
+
+def decode_packet(msg_bytes: int, t: int, rx: np.ndarray):
+    """Returns (message bytes, syndromes[t] (uint16), status 0/1/2)."""
+    rx = np.ascontiguousarray(rx, dtype=np.uint8)
+    msg = np.zeros(msg_bytes, np.uint8)
+    syn = np.zeros(t, np.uint16)
+    st = lib().oracle_decode_packet(msg_bytes, t, _ptr(rx), _ptr(msg), _ptr(syn))
+    if st < 0:
+        raise RuntimeError("oracle_decode_packet failed")
+    return msg, syn, int(st)
+
+
+def generate_packets(msg_bytes: int, t: int, seed: int, g_first: int, count: int, stride: int,
+                     p: float = 1.0, want_msg: bool = False, threads: int = 1):
+    thresh, all_, _ = channel_thresholds(p, 0.0)
+    rx = np.zeros(count * stride, np.uint8)
+    msg = np.zeros(count * msg_bytes, np.uint8) if want_msg else None
+    L = lib()
+
+    def run(r):
+        a, b = r
+        rp = ctypes.c_void_p(rx.ctypes.data + a * stride)
+        mp = None if msg is None else ctypes.c_void_p(msg.ctypes.data + a * msg_bytes)
+        if L.oracle_generate_packets(msg_bytes, t, seed & (2 ** 64 - 1), g_first + a, b - a, thresh, all_,
+                                     rp, stride, mp) != 0:
+            raise RuntimeError("oracle_generate_packets failed")
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(run, _ranges(count, threads, align=1)))
+    return rx, msg
+
+
+def decode_packets(msg_bytes: int, t: int, rx: np.ndarray, count: int, stride: int, threads: int = 1):
+    """Decode `count` packets `stride` bytes apart: (messages, syndromes[count, t], status[count])."""
+    rx = np.ascontiguousarray(rx, dtype=np.uint8)
+    msg = np.zeros(count * msg_bytes, np.uint8)
+    syn = np.zeros((count, t), np.uint16)
+    status = np.zeros(count, np.uint8)
+    L = lib()
+
+    def run(r):
+        a, b = r
+        for j in range(a, b):
+            st = L.oracle_decode_packet(msg_bytes, t, ctypes.c_void_p(rx.ctypes.data + j * stride),
+                                        ctypes.c_void_p(msg.ctypes.data + j * msg_bytes),
+                                        ctypes.c_void_p(syn.ctypes.data + j * t * 2))
+            if st < 0:
+                raise RuntimeError("oracle_decode_packet failed")
+            status[j] = st
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(run, _ranges(count, threads, align=1)))
+    return msg, syn, status

@@ -321,3 +321,165 @@ int oracle_generate(int m, uint64_t seed, uint64_t c_first, uint64_t count,
 
 /* ABI marker so tests can check they loaded the oracle, not something else. */
 int oracle_version(void) { return 1; }
+
+/* ================================================================== */
+/* The paper's own workload: one packet of      */
+/* msg_bytes message bytes is split into t segments ("splits the  */
+/* message into t segments H_1 ... H_t, where t is the error tolerance")*/
+/* and each segment is one shortened Hamming codeword with the minimal  */
+/* r of 2^r >= k + r + 1 (P:L98 |H_i| = 7 + 4 = 11, |R| = 4).           */
+/* ================================================================== */
+
+/* Segment sizes (reading R14, SPEC make_layout): the first (bits mod t)
+ * segments get ceil(bits/t) message bits, the rest floor(bits/t).  Writes
+ * seg_k[t], seg_n[t]; returns the total coded bits, or -1. */
+long oracle_packet_layout(uint32_t msg_bits, int t, uint32_t *seg_k, uint32_t *seg_n)
+{
+    if (t < 1 || msg_bits < (uint32_t)t) return -1;
+    long total = 0;
+    for (int i = 0; i < t; i++) {
+        uint32_t k = msg_bits / (uint32_t)t + ((uint32_t)i < msg_bits % (uint32_t)t ? 1u : 0u);
+        int r = oracle_parity_bit_count((int)k);
+        if (r < 0 || k + (uint32_t)r > ORACLE_MAX_N * 4u) return -1;
+        seg_k[i] = k;
+        seg_n[i] = k + (uint32_t)r;
+        total += (long)seg_n[i];
+    }
+    return total;
+}
+
+#define ORACLE_MAX_SEG 16384  /* longest shortened codeword the packet routines take */
+
+/* Syndrome of a general n-bit word (n may exceed ORACLE_MAX_N): the same
+ * definition as oracle_syndrome_bits -- bit j is the XOR over I_j -- walked
+ * position by position. */
+static int syndrome_long(int n, const uint8_t *bits)
+{
+    int r = oracle_parity_positions(n);
+    int s = 0;
+    for (int j = 0; j < r; j++) {
+        int c = 0;
+        for (int p = 1; p <= n; p++)
+            if ((p >> j) & 1) c = c ^ (bits[p - 1] & 1);
+        s = s + c * (1 << j);
+    }
+    return s;
+}
+
+static void encode_long(int n, const uint8_t *msg, uint8_t *cw)
+{
+    int r = oracle_parity_positions(n);
+    int i = 0;
+    for (int p = 1; p <= n; p++) {
+        if (is_power_of_two(p)) cw[p - 1] = 0;
+        else { cw[p - 1] = msg[i] & 1; i++; }
+    }
+    for (int j = 0; j < r; j++) {
+        int c = 0;
+        for (int p = 1; p <= n; p++)
+            if (((p >> j) & 1) && p != (1 << j)) c = c ^ cw[p - 1];
+        cw[(1 << j) - 1] = (uint8_t)c;
+    }
+}
+
+/* Encode one packet: message bits (LSB-first bytes) -> splitter -> encoder per
+ * segment -> concatenation H = H_1 + ... + H_t, LSB-first, pad bits 0. */
+int oracle_encode_packet(uint32_t msg_bytes, int t, const uint8_t *msg, uint8_t *rx)
+{
+    uint32_t seg_k[64], seg_n[64];
+    if (t > 64) return -1;
+    long total = oracle_packet_layout(msg_bytes * 8u, t, seg_k, seg_n);
+    if (total < 0) return -1;
+    static __thread uint8_t m[ORACLE_MAX_SEG], cw[ORACLE_MAX_SEG];
+    uint64_t mb = 0, cb = 0;
+    for (int i = 0; i < t; i++) {
+        if (seg_n[i] > ORACLE_MAX_SEG) return -1;
+        for (uint32_t b = 0; b < seg_k[i]; b++) m[b] = (uint8_t)get_bit(msg, mb + b);
+        encode_long((int)seg_n[i], m, cw);
+        for (uint32_t p = 0; p < seg_n[i]; p++) put_bit(rx, cb + p, cw[p]);
+        mb += seg_k[i];
+        cb += seg_n[i];
+    }
+    for (uint64_t b = cb; b < ((cb + 7) / 8) * 8; b++) put_bit(rx, b, 0);
+    return 0;
+}
+
+/* Decode one packet (Fig. 1: splitter -> ED/EC/RR per segment -> merger):
+ *   syn[i]  = syndrome of segment i;
+ *   s = 0: nothing; 1 <= s <= n_i: bit s flipped (corrected); s > n_i: the
+ *   syndrome names a position that does not exist -> uncorrectable (SPEC
+ *   detect_and_correct), the segment's bits are left as received (reading
+ *   R15) and the packet status is 2;
+ *   msg = merged message bits.  Returns the packet status: 0 clean,
+ *   1 corrected, 2 uncorrectable; -1 on a bad argument. */
+int oracle_decode_packet(uint32_t msg_bytes, int t, const uint8_t *rx, uint8_t *msg, uint16_t *syn)
+{
+    uint32_t seg_k[64], seg_n[64];
+    if (t > 64) return -1;
+    long total = oracle_packet_layout(msg_bytes * 8u, t, seg_k, seg_n);
+    if (total < 0) return -1;
+    static __thread uint8_t bits[ORACLE_MAX_SEG], m[ORACLE_MAX_SEG];
+    uint64_t mb = 0, cb = 0;
+    int status = 0;
+    for (int i = 0; i < t; i++) {
+        int n = (int)seg_n[i];
+        if (n > ORACLE_MAX_SEG) return -1;
+        for (int p = 0; p < n; p++) bits[p] = (uint8_t)get_bit(rx, cb + (uint64_t)p);   /* splitter */
+        int s = syndrome_long(n, bits);                                                 /* ED */
+        if (s != 0 && s <= n) {                                                         /* EC */
+            bits[s - 1] ^= 1;
+            if (status < 1) status = 1;
+        } else if (s > n) {
+            status = 2;
+        }
+        int k = oracle_remove_redundancy_bits(n, bits, m);                              /* RR */
+        for (int b = 0; b < k; b++) put_bit(msg, mb + (uint64_t)b, m[b]);              /* merger */
+        if (syn) syn[i] = (uint16_t)s;
+        mb += seg_k[i];
+        cb += (uint64_t)n;
+    }
+    return status;
+}
+
+/* Seeded packet channel (packets): for global
+ * packet index g, key = mix(seed + (g+1) gamma) and u(g,q) = mix(key +
+ * (q+1) gamma).  Message byte b = byte (b & 7) of u(g, b >> 3); W = number of
+ * message draws = ceil(msg_bytes / 8); segment i has an error event iff all
+ * or u(g, W + 2i) < thresh, at position 1 + umulhi(lo32(u(g, W + 2i + 1)), n_i)
+ * (one flip per segment: the paper's t-error regime).
+ * Packet j of the output starts at rx + j*stride (stride >= coded bytes);
+ * msg (nullable) gets the sent messages, msg_bytes apart.  Returns 0 / -1. */
+int oracle_generate_packets(uint32_t msg_bytes, int t, uint64_t seed, uint64_t g_first, uint64_t count,
+                            uint64_t thresh, int all, uint8_t *rx, uint64_t stride, uint8_t *msg)
+{
+    uint32_t seg_k[64], seg_n[64];
+    if (t > 64) return -1;
+    long total = oracle_packet_layout(msg_bytes * 8u, t, seg_k, seg_n);
+    if (total < 0 || stride < (uint64_t)((total + 7) / 8)) return -1;
+    static __thread uint8_t m[ORACLE_MAX_SEG / 8 * 64];
+    uint32_t W = (msg_bytes + 7) / 8;
+    for (uint64_t j = 0; j < count; j++) {
+        uint64_t g = g_first + j;
+        uint64_t key = mix64(seed + (g + 1) * 0x9E3779B97F4A7C15ULL);
+        for (uint32_t b = 0; b < msg_bytes; b++) {
+            uint64_t u = mix64(key + ((uint64_t)(b >> 3) + 1) * 0x9E3779B97F4A7C15ULL);
+            m[b] = (uint8_t)(u >> (8 * (b & 7)));
+        }
+        uint8_t *out = rx + j * stride;
+        if (oracle_encode_packet(msg_bytes, t, m, out) != 0) return -1;
+        uint64_t cb = 0;
+        for (int i = 0; i < t; i++) {
+            uint64_t ue = mix64(key + ((uint64_t)W + 2 * (uint64_t)i + 1) * 0x9E3779B97F4A7C15ULL);
+            uint64_t up = mix64(key + ((uint64_t)W + 2 * (uint64_t)i + 2) * 0x9E3779B97F4A7C15ULL);
+            if (all || ue < thresh) {
+                uint64_t p = 1 + (((up & 0xFFFFFFFFULL) * (uint64_t)seg_n[i]) >> 32);
+                uint64_t b = cb + p - 1;
+                put_bit(out, b, get_bit(out, b) ^ 1);
+            }
+            cb += seg_n[i];
+        }
+        for (uint64_t b = (uint64_t)total; b < stride * 8; b++) put_bit(out, b, 0);
+        if (msg) for (uint32_t b = 0; b < msg_bytes; b++) msg[j * msg_bytes + b] = m[b];
+    }
+    return 0;
+}

@@ -60,6 +60,17 @@ def lib() -> ctypes.CDLL:
     L.hamming_host_workspace_bytes.restype = ctypes.c_size_t
     L.hamming_decode_host.argtypes = [c_int, vp, u64, vp, vp, vp, vp, u64, c_int]
     L.hamming_decode_host.restype = c_int
+    u32 = ctypes.c_uint32
+    L.hamming_packet_coded_bytes.argtypes = [u32, c_int]
+    L.hamming_packet_coded_bytes.restype = u64
+    L.hamming_packet_layout.argtypes = [u32, c_int, vp, vp]
+    L.hamming_packet_layout.restype = c_int
+    L.hamming_decode_packets.argtypes = [u32, c_int, vp, u64, u64, vp, u64, vp, vp, vp, vp]
+    L.hamming_decode_packets.restype = c_int
+    L.hamming_encode_packets.argtypes = [u32, c_int, vp, u64, u64, vp, u64, vp]
+    L.hamming_encode_packets.restype = c_int
+    L.hamming_packet_channel_generate.argtypes = [u32, c_int, u64, u64, u64, u64, c_int, vp, u64, vp, vp]
+    L.hamming_packet_channel_generate.restype = c_int
     L.hamming_coded_bytes.argtypes = [c_int, u64]
     L.hamming_coded_bytes.restype = u64
     L.hamming_data_bytes.argtypes = [c_int, u64]

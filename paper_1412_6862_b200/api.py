@@ -170,3 +170,97 @@ def last_launch_count() -> int:
 
 def last_grid_blocks() -> int:
     return int(lib().hamming_last_grid_blocks())
+
+
+# ------------------------------------------------ packets (the paper's workload)
+def packet_layout(msg_bytes: int, t: int) -> tuple[list[int], list[int]]:
+    """(seg_k, seg_n) of a msg_bytes-byte packet split into t segments."""
+    k = (ctypes.c_uint32 * max(1, t))()
+    n = (ctypes.c_uint32 * max(1, t))()
+    check(lib().hamming_packet_layout(msg_bytes, t, k, n), "hamming_packet_layout")
+    return list(k[:t]), list(n[:t])
+
+
+def packet_coded_bytes(msg_bytes: int, t: int) -> int:
+    v = int(lib().hamming_packet_coded_bytes(msg_bytes, t))
+    if v == 0:
+        raise ValueError("bad packet shape")
+    return v
+
+
+def packet_stride(msg_bytes: int, t: int) -> int:
+    """The smallest legal rx_stride: coded bytes rounded up to 16."""
+    return (packet_coded_bytes(msg_bytes, t) + 15) // 16 * 16
+
+
+@dataclass
+class PacketDecodeResult:
+    messages: torch.Tensor             # uint8 [n_packets * msg_stride]
+    syndromes: Optional[torch.Tensor]  # uint16 as int16 storage [n_packets, t]
+    status: Optional[torch.Tensor]     # uint8 [n_packets]: 0 clean, 1 corrected, 2 uncorrectable
+    counts: torch.Tensor               # int64 [2]: segments corrected, segments uncorrectable
+
+
+def hamming_decode_packets(msg_bytes: int, t: int, rx: torch.Tensor, n_packets: int, *, rx_stride: Optional[int] = None,
+                           msg_out: Optional[torch.Tensor] = None, msg_stride: Optional[int] = None,
+                           syndromes: bool = True, status: bool = True,
+                           stream: Optional[torch.cuda.Stream] = None) -> PacketDecodeResult:
+    rx_stride = packet_stride(msg_bytes, t) if rx_stride is None else rx_stride
+    msg_stride = msg_bytes if msg_stride is None else msg_stride
+    P = int(n_packets)
+    dev = rx.device
+    if msg_out is None:
+        msg_out = torch.empty(max(1, P * msg_stride), dtype=torch.uint8, device=dev)
+    syn = torch.empty((max(1, P), t), dtype=torch.int16, device=dev) if syndromes else None
+    st = torch.empty(max(1, P), dtype=torch.uint8, device=dev) if status else None
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
+    rc = lib().hamming_decode_packets(msg_bytes, t, _dev_ptr(rx, "rx", rx_stride * P), rx_stride, P,
+                                      _dev_ptr(msg_out, "msg_out", msg_stride * P), msg_stride,
+                                      _dev_ptr(syn, "syndromes", 2 * t * P), _dev_ptr(st, "status", P),
+                                      _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
+    check(rc, "hamming_decode_packets")
+    return PacketDecodeResult(msg_out, syn, st, counts)
+
+
+decode_packets = hamming_decode_packets
+
+
+def hamming_encode_packets(msg_bytes: int, t: int, messages: torch.Tensor, n_packets: int, *,
+                           msg_stride: Optional[int] = None, rx_stride: Optional[int] = None,
+                           rx_out: Optional[torch.Tensor] = None,
+                           stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    rx_stride = packet_stride(msg_bytes, t) if rx_stride is None else rx_stride
+    msg_stride = msg_bytes if msg_stride is None else msg_stride
+    P = int(n_packets)
+    if rx_out is None:
+        rx_out = torch.empty(max(1, P * rx_stride), dtype=torch.uint8, device=messages.device)
+    rc = lib().hamming_encode_packets(msg_bytes, t, _dev_ptr(messages, "messages", msg_stride * P), msg_stride, P,
+                                      _dev_ptr(rx_out, "rx_out", rx_stride * P), rx_stride,
+                                      _stream_handle(stream, messages.device))
+    check(rc, "hamming_encode_packets")
+    return rx_out
+
+
+encode_packets = hamming_encode_packets
+
+
+def hamming_packet_channel_generate(msg_bytes: int, t: int, seed: int, g_first: int, n_packets: int, p: float = 1.0,
+                                    *, rx_stride: Optional[int] = None, want_messages: bool = False, device=None,
+                                    stream: Optional[torch.cuda.Stream] = None):
+    """Seeded received packets (one flip per segment with probability p).
+    Returns (rx, messages|None)."""
+    rx_stride = packet_stride(msg_bytes, t) if rx_stride is None else rx_stride
+    P = int(n_packets)
+    thresh, all_, _ = channel_thresholds(p, 0.0)
+    device = device if device is not None else "cuda"
+    rx = torch.empty(max(1, P * rx_stride), dtype=torch.uint8, device=device)
+    msgs = torch.empty(max(1, P * msg_bytes), dtype=torch.uint8, device=device) if want_messages else None
+    rc = lib().hamming_packet_channel_generate(msg_bytes, t, seed & (2 ** 64 - 1), g_first, P, thresh, all_,
+                                               _dev_ptr(rx, "rx", rx_stride * P), rx_stride,
+                                               _dev_ptr(msgs, "messages", msg_bytes * P),
+                                               _stream_handle(stream, rx.device))
+    check(rc, "hamming_packet_channel_generate")
+    return rx, msgs
+
+
+packet_channel_generate = hamming_packet_channel_generate

@@ -33,7 +33,9 @@ def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in (SRC, HDR))
+    import glob
+    deps = [SRC, HDR] + glob.glob(os.path.join(PKG, "csrc", "*.cuh"))
+    return any(os.path.getmtime(p) > t for p in deps)
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:

@@ -944,6 +944,8 @@ HostSlotLayout host_slot_layout(int m, uint64_t chunk, int with_syn) {
   return L;
 }
 
+#include "packets.cuh"
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1129,6 +1131,108 @@ hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void*
     if (streams[i]) cudaStreamDestroy(streams[i]);
   g_launches = launches;
   return rc;
+}
+
+// ------------------------------------------------- packets (the paper's workload)
+uint64_t hamming_packet_coded_bytes(uint32_t msg_bytes, int t) {
+  PacketGeom g;
+  if (packet_geom(msg_bytes, t, g) != HAMMING_OK) return 0;
+  return (g.coded_bits + 7) / 8;
+}
+
+hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t* seg_k, uint32_t* seg_n) {
+  PacketGeom g;
+  const hamming_status rc = packet_geom(msg_bytes, t, g);
+  if (rc != HAMMING_OK) return rc;
+  if (seg_k == nullptr || seg_n == nullptr) return set_err(HAMMING_E_NULL, "hamming_packet_layout: NULL output");
+  for (int i = 0; i < t; ++i) {
+    seg_k[i] = g.k[i];
+    seg_n[i] = g.n[i];
+  }
+  return HAMMING_OK;
+}
+
+static hamming_status packet_common(uint32_t msg_bytes, int t, uint64_t pk_stride, const void* pk, PacketGeom& g,
+                                    const char* who) {
+  const hamming_status rc = packet_geom(msg_bytes, t, g);
+  if (rc != HAMMING_OK) return rc;
+  if (pk_stride < g.in_bytes || (pk_stride & 15u) != 0) {
+    snprintf(g_err, sizeof(g_err), "%s: packet stride must be a multiple of 16 and >= %u", who, g.in_bytes);
+    return HAMMING_E_ARG;
+  }
+  if (!aligned16(pk)) return set_err(HAMMING_E_MISALIGNED, "packets: packet buffer must be 16-byte aligned");
+  return HAMMING_OK;
+}
+
+hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void* rx_dev, uint64_t rx_stride,
+                                      uint64_t n_packets, void* msg_dev, uint64_t msg_stride,
+                                      uint16_t* syndromes_dev, uint8_t* status_dev,
+                                      unsigned long long* counts_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  PacketGeom g;
+  hamming_status rc = packet_common(msg_bytes, t, rx_stride, rx_dev, g, "hamming_decode_packets");
+  if (rc != HAMMING_OK) return rc;
+  if (n_packets > 0 && (rx_dev == nullptr || msg_dev == nullptr))
+    return set_err(HAMMING_E_NULL, "hamming_decode_packets: NULL buffer");
+  if (msg_stride < msg_bytes) return set_err(HAMMING_E_ARG, "hamming_decode_packets: msg_stride < msg_bytes");
+  if (n_packets > 0 && ranges_overlap(rx_dev, rx_stride * n_packets, msg_dev, msg_stride * n_packets))
+    return set_err(HAMMING_E_OVERLAP, "hamming_decode_packets: buffers overlap");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (counts_dev != nullptr) {
+    const cudaError_t e = cudaMemsetAsync(counts_dev, 0, 2 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counts)");
+  }
+  PacketArgs a{};
+  a.in = static_cast<const uint8_t*>(rx_dev);
+  a.in_stride = rx_stride;
+  a.out = static_cast<uint8_t*>(msg_dev);
+  a.out_stride = msg_stride;
+  a.syn = syndromes_dev;
+  a.status = status_dev;
+  a.counts = counts_dev;
+  a.n_packets = n_packets;
+  return launch_packets<kPktDecode>(g, a, st);
+}
+
+hamming_status hamming_encode_packets(uint32_t msg_bytes, int t, const void* msg_dev, uint64_t msg_stride,
+                                      uint64_t n_packets, void* rx_dev, uint64_t rx_stride, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  PacketGeom g;
+  hamming_status rc = packet_common(msg_bytes, t, rx_stride, rx_dev, g, "hamming_encode_packets");
+  if (rc != HAMMING_OK) return rc;
+  if (n_packets > 0 && (rx_dev == nullptr || msg_dev == nullptr))
+    return set_err(HAMMING_E_NULL, "hamming_encode_packets: NULL buffer");
+  if (msg_stride < msg_bytes) return set_err(HAMMING_E_ARG, "hamming_encode_packets: msg_stride < msg_bytes");
+  PacketArgs a{};
+  a.in = static_cast<const uint8_t*>(msg_dev);
+  a.in_stride = msg_stride;
+  a.out = static_cast<uint8_t*>(rx_dev);
+  a.out_stride = rx_stride;
+  a.n_packets = n_packets;
+  return launch_packets<kPktEncode>(g, a, static_cast<cudaStream_t>(stream));
+}
+
+hamming_status hamming_packet_channel_generate(uint32_t msg_bytes, int t, uint64_t seed, uint64_t g_first,
+                                               uint64_t n_packets, uint64_t thresh, int all, void* rx_dev,
+                                               uint64_t rx_stride, void* msg_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  PacketGeom g;
+  hamming_status rc = packet_common(msg_bytes, t, rx_stride, rx_dev, g, "hamming_packet_channel_generate");
+  if (rc != HAMMING_OK) return rc;
+  if (n_packets > 0 && rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_packet_channel_generate: NULL rx");
+  PacketArgs a{};
+  a.out = static_cast<uint8_t*>(rx_dev);
+  a.out_stride = rx_stride;
+  a.n_packets = n_packets;
+  a.seed = seed;
+  a.g_first = g_first;
+  a.thresh = thresh;
+  a.all = all;
+  a.gen_msg = static_cast<uint8_t*>(msg_dev);
+  return launch_packets<kPktGenerate>(g, a, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

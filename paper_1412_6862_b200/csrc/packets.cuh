@@ -1,0 +1,365 @@
+// paper_1412_6862_b200/csrc/packets.cuh -- the paper's own workload (SURVEY.md
+// 8(f) row f2), included into hamming.cu's anonymous namespace.
+//
+// A packet of msg_bytes message bytes is split into t segments ("splits
+// the message into t segments H_1 ... H_t, where t is the error tolerance";
+// near-equal, larger first: DESIGN.md reading R14) and every segment is one
+// SHORTENED Hamming codeword: k_i message bits, the minimal r_i with
+// 2^r >= k + r + 1 ("|H_i| = 7+4 = 11 bits and |R| = 4"), n_i = k_i + r_i,
+// n up to 8013 bits on the paper's grid (M = 400..2000 B, t = 2..6).
+// The encoded packet is H = H_1 + ... + H_t, LSB-first (reading R4).
+//
+// GPU design: one warp per packet (grid-stride over packets), the packet
+// staged in shared memory with coalesced 128-bit loads.
+// Per segment:
+//   syndrome (the checksum vector): position p = 32 j + b, so
+//     s = XOR_j [32 j * parity(x_j)]  ^  S5( XOR_j x_j ),
+//   where x_j is the 32-position chunk j and S5(x) = XOR of the bit indices
+//   of x (five POPCs).  S5 is linear, so each lane XORs its chunks and pays
+//   one POPC per chunk for the parity; one warp XOR-reduction; S5 once.
+//   ED/EC: s = 0 clean; 1 <= s <= n flip bit s (one lane, in shared memory);
+//   s > n names a non-existent position: uncorrectable, bits left as received
+//   (reading R15; SPEC detect_and_correct).
+//   RR + merger: data index d of position p in run j (2^j < p < 2^(j+1)) is
+//   p - j - 2, so every 32-bit word of the message is 1..3 funnel-shifted
+//   slices of the packet stream; lanes build consecutive message words.
+
+constexpr int kPktMaxSeg = 16;
+constexpr int kPktMaxMsgBytes = 4096;
+constexpr int kPktWarps = 8;
+
+struct PacketGeom {
+  uint32_t msg_bytes, t, coded_bits, in_bytes;  // in_bytes = coded bytes rounded up to 16
+  uint32_t in_cap, msg_cap;                     // per-warp shared buffer sizes (bytes, 16-aligned)
+  uint32_t off[kPktMaxSeg];                     // segment bit offset in the packet stream
+  uint32_t n[kPktMaxSeg], k[kPktMaxSeg], r[kPktMaxSeg];
+  uint32_t moff[kPktMaxSeg];                    // segment bit offset in the message
+};
+
+// host: the layout (same rule as the oracle's, written independently)
+hamming_status packet_geom(uint32_t msg_bytes, int t, PacketGeom& g) {
+  if (t < 1 || t > kPktMaxSeg) return set_err(HAMMING_E_ARG, "packets: t must be in [1, 16]");
+  if (msg_bytes < 1 || msg_bytes > kPktMaxMsgBytes)
+    return set_err(HAMMING_E_ARG, "packets: msg_bytes must be in [1, 4096]");
+  const uint32_t bits = msg_bytes * 8u;
+  if (bits < static_cast<uint32_t>(t)) return set_err(HAMMING_E_ARG, "packets: fewer message bits than segments");
+  memset(&g, 0, sizeof(g));
+  g.msg_bytes = msg_bytes;
+  g.t = static_cast<uint32_t>(t);
+  uint32_t off = 0, moff = 0;
+  for (int i = 0; i < t; ++i) {
+    const uint32_t k = bits / t + (static_cast<uint32_t>(i) < bits % t ? 1u : 0u);
+    uint32_t r = 0;
+    while ((1u << r) < k + r + 1) ++r;
+    g.k[i] = k;
+    g.r[i] = r;
+    g.n[i] = k + r;
+    g.off[i] = off;
+    g.moff[i] = moff;
+    off += k + r;
+    moff += k;
+  }
+  g.coded_bits = off;
+  g.in_bytes = ((off + 7) / 8 + 15) / 16 * 16;
+  g.in_cap = g.in_bytes + 16;                    // slack: funnel reads one word past the end
+  g.msg_cap = (msg_bytes + 15) / 16 * 16 + 16;
+  return HAMMING_OK;
+}
+
+// 32 stream bits starting at bit o of a shared-memory word array.
+__device__ __forceinline__ uint32_t sm_bits32(const uint32_t* w, uint32_t o) {
+  const uint32_t q = o >> 5, r = o & 31u;
+  const uint32_t a = w[q];
+  return r ? __funnelshift_r(a, w[q + 1], r) : a;
+}
+
+__device__ __forceinline__ uint32_t low_mask(uint32_t c) { return c >= 32 ? 0xFFFFFFFFu : ((1u << c) - 1u); }
+
+// XOR of the indices of the set bits of a 32-bit word (5 POPCs).
+__device__ __forceinline__ uint32_t xor_of_indices(uint32_t x) {
+  return (static_cast<uint32_t>(__popc(x & 0xAAAAAAAAu) & 1) << 0) |
+         (static_cast<uint32_t>(__popc(x & 0xCCCCCCCCu) & 1) << 1) |
+         (static_cast<uint32_t>(__popc(x & 0xF0F0F0F0u) & 1) << 2) |
+         (static_cast<uint32_t>(__popc(x & 0xFF00FF00u) & 1) << 3) |
+         (static_cast<uint32_t>(__popc(x & 0xFFFF0000u) & 1) << 4);
+}
+
+// Syndrome of segment (off, n) of the packet stream `w`: positions 1..n are
+// stream bits off .. off+n-1.  Warp-collective; every lane returns s.
+__device__ __forceinline__ uint32_t segment_syndrome(const uint32_t* w, uint32_t off, uint32_t n, int lane) {
+  const uint32_t chunks = (n + 32) / 32;  // positions 0..n
+  uint32_t X = 0, P = 0;
+  for (uint32_t j = lane; j < chunks; j += 32) {
+    // chunk j = positions 32j .. 32j+31 = stream bits off + 32j - 1 ...
+    uint32_t x;
+    if (j == 0) x = (off == 0 ? (w[0] << 1) : sm_bits32(w, off - 1)) & ~1u;  // position 0 is not a position
+    else x = sm_bits32(w, off + 32 * j - 1);
+    const uint32_t last = n - 32 * j;  // highest position index inside this chunk, if < 32
+    if (last < 31) x &= low_mask(last + 1);
+    X ^= x;
+    P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
+  }
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+    P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+  }
+  return P ^ xor_of_indices(X);
+}
+
+// Data index -> run: the data bits of run j (positions 2^j+1 .. 2^(j+1)-1) are
+// d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2.
+__device__ __forceinline__ uint32_t run_of(uint32_t d) {
+  uint32_t j = 1;
+  while ((2u << j) - j - 2 <= d) ++j;  // first d of run j+1 is 2^(j+1) - (j+1) - 1
+  return j;
+}
+
+// Message word mw (bits 32 mw .. 32 mw + 31 of the packet message) restricted
+// to segment (off, k, moff): the data bits of that segment, RR'd, in place.
+__device__ __forceinline__ uint32_t segment_msg_word(const uint32_t* w, uint32_t off, uint32_t k, uint32_t moff,
+                                                     uint32_t mw) {
+  const uint32_t b0 = max(32u * mw, moff), b1 = min(32u * mw + 32u, moff + k);
+  uint32_t out = 0;
+  uint32_t b = b0;
+  uint32_t d = b - moff;
+  uint32_t j = run_of(d);
+  while (b < b1) {
+    const uint32_t run_end = (2u << j) - j - 2;  // first data index of the next run
+    const uint32_t take = min(b1, moff + run_end) - b;
+    const uint32_t src = off + d + j + 1;       // stream bit of position d + j + 2
+    out |= (sm_bits32(w, src) & low_mask(take)) << (b - 32u * mw);
+    b += take;
+    d += take;
+    ++j;
+  }
+  return out;
+}
+
+// Encoder side: codeword word cw (positions 32 cw .. 32 cw + 31) of segment
+// (k, moff) built from the message words `msg` -- data positions only (parity
+// positions and position 0 left 0).
+__device__ __forceinline__ uint32_t segment_code_word(const uint32_t* msg, uint32_t n, uint32_t moff, uint32_t cw) {
+  uint32_t out = 0;
+  uint32_t p = max(32u * cw, 3u), p1 = min(32u * cw + 32u, n + 1);
+  while (p < p1) {
+    const uint32_t j = 31u - __clz(p);  // 2^j <= p < 2^(j+1)
+    if (p == (1u << j)) {               // parity position
+      ++p;
+      continue;
+    }
+    const uint32_t run_end = min(p1, 2u << j);
+    const uint32_t take = run_end - p;
+    const uint32_t d = p - j - 2;
+    out |= (sm_bits32(msg, moff + d) & low_mask(take)) << (p - 32u * cw);
+    p = run_end;
+  }
+  return out;
+}
+
+// Decode the packet held in shared memory `w` into the shared message buffer
+// `mbuf` (zeroed here); returns (per lane 0) the packet status and writes
+// syndromes.  Warp-collective.
+__device__ __forceinline__ uint32_t decode_packet_warp(const PacketGeom& g, uint32_t* w, uint32_t* mbuf, int lane,
+                                                       uint16_t* syn_out, uint32_t& n_corr, uint32_t& n_fail) {
+  const uint32_t mwords = (g.msg_bytes + 3) / 4;
+  for (uint32_t i = lane; i < mwords; i += 32) mbuf[i] = 0;
+  uint32_t status = 0;
+  for (uint32_t i = 0; i < g.t; ++i) {
+    const uint32_t off = g.off[i], n = g.n[i], k = g.k[i], moff = g.moff[i];
+    const uint32_t s = segment_syndrome(w, off, n, lane);
+    if (s != 0 && s <= n) {  // EC: flip position s (stream bit off + s - 1)
+      if (lane == 0) {
+        const uint32_t b = off + s - 1;
+        w[b >> 5] ^= 1u << (b & 31);
+      }
+      status = max(status, 1u);
+      ++n_corr;
+    } else if (s > n) {
+      status = 2;
+      ++n_fail;
+    }
+    __syncwarp();
+    if (syn_out != nullptr && lane == 0) syn_out[i] = static_cast<uint16_t>(s);
+    // RR + merger: message words touched by this segment
+    const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
+    for (uint32_t mw = mw0 + lane; mw < mw1; mw += 32) mbuf[mw] |= segment_msg_word(w, off, k, moff, mw);
+    __syncwarp();
+  }
+  return status;
+}
+
+// Encode the message in shared memory `msg` into the packet stream `w`
+// (zeroed here, in_cap bytes) -- the "exact reverse process": data at
+// the non-power-of-two positions, then parity bit 2^q = bit q of the syndrome
+// of the data-only word (even parity over every I_q).  Warp-collective.
+__device__ __forceinline__ void encode_packet_warp(const PacketGeom& g, const uint32_t* msg, uint32_t* w, int lane) {
+  for (uint32_t i = lane; i < g.in_cap / 4; i += 32) w[i] = 0;
+  __syncwarp();
+  for (uint32_t i = 0; i < g.t; ++i) {
+    const uint32_t off = g.off[i], n = g.n[i], moff = g.moff[i], r = g.r[i];
+    const uint32_t words = (n + 32) / 32;  // position words 0 .. n/32
+    uint32_t X = 0, P = 0;
+    for (uint32_t cw = lane; cw < words; cw += 32) {
+      uint32_t x = segment_code_word(msg, n, moff, cw);  // bit b = position 32cw + b
+      X ^= x;
+      P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * cw);
+      // position p sits at stream bit off + p - 1
+      uint32_t base;
+      if (cw == 0) {
+        x >>= 1;  // drop position 0
+        base = off;
+      } else {
+        base = off + 32 * cw - 1;
+      }
+      const uint32_t q = base >> 5, rr = base & 31u;
+      if (x) {
+        atomicOr(&w[q], x << rr);
+        if (rr) atomicOr(&w[q + 1], x >> (32 - rr));
+      }
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+    }
+    const uint32_t s = P ^ xor_of_indices(X);  // syndrome of the data-only word
+    if (static_cast<uint32_t>(lane) < r && ((s >> lane) & 1u)) {
+      const uint32_t b = off + (1u << lane) - 1;
+      atomicOr(&w[b >> 5], 1u << (b & 31));
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ uint64_t pkt_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+enum PacketMode { kPktDecode = 0, kPktEncode = 1, kPktGenerate = 2 };
+
+struct PacketArgs {
+  const uint8_t* in;   // decode: received packets; encode: messages
+  uint64_t in_stride;
+  uint8_t* out;        // decode: messages; encode/generate: packets
+  uint64_t out_stride;
+  uint16_t* syn;       // decode: n_packets * t syndromes (nullable)
+  uint8_t* status;     // decode: n_packets statuses (nullable)
+  unsigned long long* counts;  // decode: [corrected segments, uncorrectable segments] (nullable)
+  uint64_t n_packets;
+  // generate
+  uint64_t seed, g_first, thresh;
+  int all;
+  uint8_t* gen_msg;    // generate: sent messages (nullable), msg_bytes apart
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kPktWarps * 32)
+    packets_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ PacketArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ unsigned long long cta_counts[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wb = smem + warp * (g.in_cap + g.msg_cap);
+  uint32_t* w = reinterpret_cast<uint32_t*>(wb);                 // packet stream
+  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + g.in_cap);   // message
+  if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  uint32_t n_corr = 0, n_fail = 0;
+  for (uint64_t pk = gw; pk < a.n_packets; pk += nw) {
+    if constexpr (MODE == kPktDecode) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.in + pk * a.in_stride);
+      for (uint32_t i = lane; i < g.in_bytes / 16; i += 32) reinterpret_cast<uint4*>(w)[i] = src[i];
+      if (lane < 4) w[g.in_bytes / 4 + lane] = 0;
+      __syncwarp();
+      const uint32_t st = decode_packet_warp(g, w, mbuf, lane, a.syn ? a.syn + pk * g.t : nullptr, n_corr, n_fail);
+      if (a.status != nullptr && lane == 0) a.status[pk] = static_cast<uint8_t>(st);
+      uint8_t* dst = a.out + pk * a.out_stride;
+      if (((reinterpret_cast<uintptr_t>(a.out) | a.out_stride | g.msg_bytes) & 15u) == 0) {
+        for (uint32_t i = lane; i < g.msg_bytes / 16; i += 32)
+          reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
+      } else {
+        const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[i];
+      }
+      __syncwarp();
+    } else {
+      uint8_t* mb = reinterpret_cast<uint8_t*>(mbuf);
+      if constexpr (MODE == kPktEncode) {
+        const uint8_t* src = a.in + pk * a.in_stride;
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) mb[i] = src[i];
+      } else {
+        const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
+        for (uint32_t q = lane; q < (g.msg_bytes + 7) / 8; q += 32) {
+          const uint64_t u = pkt_mix(key + (static_cast<uint64_t>(q) + 1) * 0x9E3779B97F4A7C15ull);
+          for (uint32_t b = 0; b < 8 && 8 * q + b < g.msg_bytes; ++b) mb[8 * q + b] = static_cast<uint8_t>(u >> (8 * b));
+        }
+      }
+      for (uint32_t i = g.msg_bytes + lane; i < g.msg_cap; i += 32) mb[i] = 0;
+      __syncwarp();
+      encode_packet_warp(g, mbuf, w, lane);
+      if constexpr (MODE == kPktGenerate) {
+        const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
+        const uint32_t W = (g.msg_bytes + 7) / 8;
+        if (lane < static_cast<int>(g.t)) {
+          const uint64_t ue = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 1) * 0x9E3779B97F4A7C15ull);
+          const uint64_t up = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 2) * 0x9E3779B97F4A7C15ull);
+          if (a.all || ue < a.thresh) {
+            const uint32_t p = 1u + __umulhi(static_cast<uint32_t>(up), g.n[lane]);
+            const uint32_t b = g.off[lane] + p - 1;
+            atomicXor(&w[b >> 5], 1u << (b & 31));
+          }
+        }
+        __syncwarp();
+        if (a.gen_msg != nullptr) {
+          uint8_t* gm = a.gen_msg + pk * g.msg_bytes;
+          for (uint32_t i = lane; i < g.msg_bytes; i += 32) gm[i] = mb[i];
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a.out + pk * a.out_stride);
+      for (uint32_t i = lane; i < g.in_bytes / 16; i += 32) dst[i] = reinterpret_cast<const uint4*>(w)[i];
+      __syncwarp();
+    }
+  }
+  if constexpr (MODE == kPktDecode) {
+    if (a.counts != nullptr) {
+      // s is warp-uniform, so every lane holds the warp's counts: lane 0 adds them
+      if (lane == 0) {
+        if (n_corr) atomicAdd(&cta_counts[0], static_cast<unsigned long long>(n_corr));
+        if (n_fail) atomicAdd(&cta_counts[1], static_cast<unsigned long long>(n_fail));
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (cta_counts[0]) atomicAdd(&a.counts[0], cta_counts[0]);
+        if (cta_counts[1]) atomicAdd(&a.counts[1], cta_counts[1]);
+      }
+    }
+  }
+}
+
+template <int MODE>
+hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const size_t smem = static_cast<size_t>(kPktWarps) * (g.in_cap + g.msg_cap);
+  auto kfn = packets_kernel<MODE>;
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kPktWarps * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets)");
+  const uint64_t want = (a.n_packets + kPktWarps - 1) / kPktWarps;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+  if (grid > 0) {
+    kfn<<<grid, kPktWarps * 32, smem, st>>>(g, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "packets kernel launch");
+  }
+  g_launches = grid > 0 ? 1 : 0;
+  g_grid = grid;
+  return HAMMING_OK;
+}

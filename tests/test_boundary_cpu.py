@@ -114,3 +114,27 @@ def test_product_package_never_touches_the_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle", text, re.M), f
                 assert "liboracle" not in text, f
                 assert "oracle.c" not in text or f.endswith(".cu"), f
+
+
+def test_packet_entry_point_validation(L):
+    assert L.hamming_packet_coded_bytes(0, 2) == 0
+    assert L.hamming_packet_coded_bytes(400, 0) == 0
+    assert L.hamming_packet_coded_bytes(400, 17) == 0
+    assert L.hamming_packet_coded_bytes(4097, 2) == 0
+    assert L.hamming_packet_coded_bytes(2000, 2) == (2 * 8013 + 7) // 8
+    cb = ham.packet_coded_bytes(400, 3)
+    stride = ham.packet_stride(400, 3)
+    assert stride % 16 == 0 and stride >= cb
+    big = 1 << 30
+    # stride too small / not a multiple of 16 / misaligned / NULL / overlap
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), 16, 4, ctypes.c_void_p(FAKE + big), 400,
+                                    None, None, None, None) == 7
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), stride + 8, 4, ctypes.c_void_p(FAKE + big), 400,
+                                    None, None, None, None) == 7
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE + 8), stride, 4, ctypes.c_void_p(FAKE + big), 400,
+                                    None, None, None, None) == 3
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), stride, 4, None, 400, None, None, None, None) == 2
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), stride, 4, ctypes.c_void_p(FAKE + 64), 400,
+                                    None, None, None, None) == 4
+    assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), stride, 4, ctypes.c_void_p(FAKE + big), 399,
+                                    None, None, None, None) == 7

@@ -1,0 +1,104 @@
+"""GPU parity (-m gpu) for the paper's own workload:
+packets of M message bytes split into t shortened-Hamming segments
+ -- GPU decode/encode/generator against the CPU oracle,
+bit for bit, including uncorrectable syndromes and miscorrections."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1412_6862_b200 as ham
+
+pytestmark = pytest.mark.gpu
+
+GRID = [(M, t) for M in (400, 800, 1200, 1600, 2000) for t in (2, 3, 4, 5, 6)]
+EDGE = [(1, 1), (1, 8), (13, 3), (16, 16), (1024, 1), (999, 7)]
+
+
+def gpu_decode(M, t, rx_np, P, stride):
+    rx = torch.from_numpy(rx_np).cuda()
+    res = ham.decode_packets(M, t, rx, P, rx_stride=stride)
+    torch.cuda.synchronize()
+    return (res.messages.cpu().numpy()[: P * M], res.syndromes.cpu().numpy().view(np.uint16)[:P],
+            res.status.cpu().numpy()[:P], res.counts.cpu().numpy())
+
+
+@pytest.mark.parametrize("M,t", GRID + EDGE)
+def test_generator_matches_oracle(oracle, M, t):
+    stride = ham.packet_stride(M, t)
+    P = 37
+    want, wmsg = oracle.generate_packets(M, t, 0xC0DE, 5, P, stride, p=0.7, want_msg=True)
+    got, gmsg = ham.packet_channel_generate(M, t, 0xC0DE, 5, P, p=0.7, want_messages=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy()[: P * stride], want)
+    assert np.array_equal(gmsg.cpu().numpy()[: P * M], wmsg)
+
+
+@pytest.mark.parametrize("M,t", GRID + EDGE)
+def test_decode_matches_oracle(oracle, M, t):
+    stride = ham.packet_stride(M, t)
+    P = 53
+    rx, msg = oracle.generate_packets(M, t, 0xBEE + M + t, 0, P, stride, p=1.0, want_msg=True)
+    wm, ws, wst = oracle.decode_packets(M, t, rx, P, stride)
+    gm, gs, gst, cnt = gpu_decode(M, t, rx, P, stride)
+    assert np.array_equal(gm, wm) and np.array_equal(gs, ws) and np.array_equal(gst, wst)
+    assert np.array_equal(gm, msg)                       # one error per segment: all corrected
+    assert cnt.tolist() == [int((ws > 0).sum()), 0]
+
+
+@pytest.mark.parametrize("M,t", [(400, 2), (400, 6), (2000, 2), (13, 3), (1, 1), (16, 16), (999, 7)])
+def test_random_received_packets(oracle, M, t):
+    """Uniformly random received bits: many segments carry syndromes beyond
+    n (uncorrectable) or miscorrect; GPU and oracle must agree exactly."""
+    stride = ham.packet_stride(M, t)
+    P = 64
+    rng = np.random.default_rng(M * 31 + t)
+    rx = rng.integers(0, 256, P * stride, dtype=np.uint8)
+    cb = ham.packet_coded_bytes(M, t)
+    wm, ws, wst = oracle.decode_packets(M, t, rx, P, stride)
+    gm, gs, gst, cnt = gpu_decode(M, t, rx, P, stride)
+    assert np.array_equal(gm, wm) and np.array_equal(gs, ws) and np.array_equal(gst, wst)
+    k, n = ham.packet_layout(M, t)
+    n = np.array(n)
+    assert cnt.tolist() == [int(((ws > 0) & (ws <= n)).sum()), int((ws > n).sum())]
+    if t <= 6 and M >= 400:
+        assert (wst == 2).any()   # the uncorrectable path is exercised
+
+
+@pytest.mark.parametrize("M,t", [(400, 3), (2000, 6), (13, 3), (4096, 16)])
+def test_encode_matches_oracle(oracle, M, t):
+    stride = ham.packet_stride(M, t)
+    P = 20
+    rng = np.random.default_rng(M + t)
+    msgs = rng.integers(0, 256, P * M, dtype=np.uint8)
+    got = ham.encode_packets(M, t, torch.from_numpy(msgs).cuda(), P).cpu().numpy()
+    cb = ham.packet_coded_bytes(M, t)
+    for j in range(P):
+        if oracle.packet_layout(8 * M, t)[1][0] <= 16384:
+            want = oracle.encode_packet(M, t, msgs[j * M:(j + 1) * M])
+            assert np.array_equal(got[j * stride: j * stride + cb], want)
+        assert not got[j * stride + cb:(j + 1) * stride].any()
+    gm, gs, gst, cnt = gpu_decode(M, t, got, P, stride)
+    assert np.array_equal(gm, msgs) and not gs.any() and not gst.any()
+
+
+def test_strided_messages_and_no_outputs():
+    M, t, P = 400, 4, 10
+    rx, msg = ham.packet_channel_generate(M, t, 1, 0, P, p=1.0, want_messages=True)
+    out = torch.zeros(P * 512, dtype=torch.uint8, device="cuda")
+    res = ham.decode_packets(M, t, rx, P, msg_out=out, msg_stride=512, syndromes=False, status=False)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(P, 512)
+    assert np.array_equal(o[:, :M].reshape(-1), msg.cpu().numpy()[: P * M]) and not o[:, M:].any()
+    assert res.counts.cpu().tolist() == [P * t, 0]
+
+
+@pytest.mark.parametrize("M,t", [(2048, 1), (4096, 1), (4096, 16), (4096, 5)])
+def test_longest_segments_roundtrip(M, t):
+    """Segments beyond the oracle's size limit (n up to 32784): encode -> one
+    flip per segment -> decode recovers every message (closed-form check)."""
+    P = 16
+    rx, msg = ham.packet_channel_generate(M, t, 77, 0, P, p=1.0, want_messages=True)
+    res = ham.decode_packets(M, t, rx, P)
+    torch.cuda.synchronize()
+    assert torch.equal(res.messages[: P * M], msg[: P * M])
+    assert (res.status[:P] == 1).all() and res.counts.cpu().tolist() == [P * t, 0]
