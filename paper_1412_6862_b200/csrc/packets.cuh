@@ -108,11 +108,12 @@ __device__ __forceinline__ uint32_t segment_syndrome(const uint32_t* w, uint32_t
 }
 
 // Data index -> run: the data bits of run j (positions 2^j+1 .. 2^(j+1)-1) are
-// d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2.
+// d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2.  Closed form
+// j = floor(log2(d + floor(log2(d + 2)) + 2)) (checked exhaustively for
+// d < 200000, far past the largest segment).
 __device__ __forceinline__ uint32_t run_of(uint32_t d) {
-  uint32_t j = 1;
-  while ((2u << j) - j - 2 <= d) ++j;  // first d of run j+1 is 2^(j+1) - (j+1) - 1
-  return j;
+  const uint32_t j0 = 31u - __clz(d + 2);
+  return 31u - __clz(d + j0 + 2);
 }
 
 // Message word mw (bits 32 mw .. 32 mw + 31 of the packet message) restricted
@@ -120,18 +121,22 @@ __device__ __forceinline__ uint32_t run_of(uint32_t d) {
 __device__ __forceinline__ uint32_t segment_msg_word(const uint32_t* w, uint32_t off, uint32_t k, uint32_t moff,
                                                      uint32_t mw) {
   const uint32_t b0 = max(32u * mw, moff), b1 = min(32u * mw + 32u, moff + k);
+  uint32_t d = b0 - moff;
+  uint32_t j = run_of(d);
+  uint32_t run_end = (2u << j) - j - 2;  // first data index of the next run
+  if (b1 - moff <= run_end) {            // one run: one funnel-shifted slice
+    const uint32_t x = sm_bits32(w, off + d + j + 1);
+    return (b1 - b0 == 32u) ? x : ((x & low_mask(b1 - b0)) << (b0 - 32u * mw));
+  }
   uint32_t out = 0;
   uint32_t b = b0;
-  uint32_t d = b - moff;
-  uint32_t j = run_of(d);
   while (b < b1) {
-    const uint32_t run_end = (2u << j) - j - 2;  // first data index of the next run
     const uint32_t take = min(b1, moff + run_end) - b;
-    const uint32_t src = off + d + j + 1;       // stream bit of position d + j + 2
-    out |= (sm_bits32(w, src) & low_mask(take)) << (b - 32u * mw);
+    out |= (sm_bits32(w, off + d + j + 1) & low_mask(take)) << (b - 32u * mw);
     b += take;
     d += take;
     ++j;
+    run_end = (2u << j) - j - 2;
   }
   return out;
 }

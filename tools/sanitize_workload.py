@@ -1,0 +1,28 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck): every decode shape with ragged tails, encode, generate and the
+host pipeline, at sizes that keep the sanitizer fast."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1412_6862_b200 as ham  # noqa: E402
+
+for m in (2, 3, 4, 5, 6):
+    for N in (1, 1023, 3 * 1024 + 77, 20_000):
+        rx = ham.channel_generate(m, 7, 0, N, p=0.3, q2=0.3)
+        exact = torch.empty(ham.coded_bytes(m, N), dtype=torch.uint8, device="cuda")
+        exact.copy_(rx[: exact.numel()])
+        res = ham.decode(m, exact, N)
+        ham.decode(m, exact, N, syndromes=False)
+        data = torch.empty(ham.data_bytes(m, N), dtype=torch.uint8, device="cuda")
+        data.copy_(res.data[: data.numel()])
+        ham.encode(m, data, N)
+        torch.cuda.synchronize()
+    N = 5 * 1024 + 3
+    rx = ham.channel_generate(m, 9, 0, N, p=0.2).cpu()
+    ws = torch.empty(ham.host_workspace_bytes(m, 2048, 2, True), dtype=torch.uint8, device="cuda")
+    ham.decode_host(m, rx, N, torch.empty(ham.data_bytes(m, N), dtype=torch.uint8),
+                    torch.empty(N, dtype=torch.uint8), ws, chunk_codewords=2048, n_streams=2)
+print("sanitize workload done")
