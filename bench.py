@@ -193,7 +193,7 @@ def run_reference(args):
     probe = 1 << 15
     t, _ = cpu_oracle_run(m, cfg["p"], cfg["q2"], probe, threads)
     total_steps = args.steps + args.warmup
-    n_cw = int(max(probe, probe * min(20.0, 120.0 / total_steps) / max(t, 1e-6))) // 1024 * 1024
+    n_cw = int(max(probe, probe * min(5.0, 60.0 / total_steps) / max(t, 1e-6))) // 1024 * 1024
     import oracle
     rx, _, _ = oracle.generate(m, SEED, 0, n_cw, p=cfg["p"], q2=cfg["q2"], threads=threads)
     for _ in range(args.warmup):

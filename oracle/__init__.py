@@ -146,8 +146,9 @@ def decode(m: int, rx: np.ndarray, count: int, want_syndromes: bool = True):
     rx = np.ascontiguousarray(rx, dtype=np.uint8)
     if rx.size < coded_bytes(m, count):
         raise ValueError("decode: rx too short")
-    data = np.zeros(data_bytes(m, count), np.uint8)
-    syn = np.zeros(count, np.uint8) if want_syndromes else None
+    # outputs start as 0xFF: the oracle must write every data bit and every pad bit itself
+    data = np.full(data_bytes(m, count), 0xFF, np.uint8)
+    syn = np.full(count, 0xFF, np.uint8) if want_syndromes else None
     cnt = ctypes.c_uint64(0)
     st = lib().oracle_decode(m, _ptr(rx), count, _ptr(data), _ptr(syn), ctypes.byref(cnt))
     if st != 0:
@@ -167,8 +168,8 @@ def decode_mt(m: int, rx: np.ndarray, count: int, threads: int, want_syndromes: 
     releases the GIL).  Bit-identical to decode()."""
     n, k = code_nk(m)
     rx = np.ascontiguousarray(rx, dtype=np.uint8)
-    data = np.zeros(data_bytes(m, count), np.uint8)
-    syn = np.zeros(count, np.uint8) if want_syndromes else None
+    data = np.full(data_bytes(m, count), 0xFF, np.uint8)
+    syn = np.full(count, 0xFF, np.uint8) if want_syndromes else None
     L = lib()
 
     def run(r):

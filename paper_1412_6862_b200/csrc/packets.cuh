@@ -61,16 +61,15 @@ hamming_status packet_geom(uint32_t msg_bytes, int t, PacketGeom& g) {
   }
   g.coded_bits = off;
   g.in_bytes = ((off + 7) / 8 + 15) / 16 * 16;
-  g.in_cap = g.in_bytes + 16;                    // slack: funnel reads one word past the end
+  g.in_cap = g.in_bytes + 32;  // 16-byte front pad (decode) + slack for funnel reads past the end
   g.msg_cap = (msg_bytes + 15) / 16 * 16 + 16;
   return HAMMING_OK;
 }
 
 // 32 stream bits starting at bit o of a shared-memory word array.
 __device__ __forceinline__ uint32_t sm_bits32(const uint32_t* w, uint32_t o) {
-  const uint32_t q = o >> 5, r = o & 31u;
-  const uint32_t a = w[q];
-  return r ? __funnelshift_r(a, w[q + 1], r) : a;
+  const uint32_t q = o >> 5;
+  return __funnelshift_r(w[q], w[q + 1], o & 31u);  // shift 0 returns w[q]
 }
 
 __device__ __forceinline__ uint32_t low_mask(uint32_t c) { return c >= 32 ? 0xFFFFFFFFu : ((1u << c) - 1u); }
@@ -84,18 +83,23 @@ __device__ __forceinline__ uint32_t xor_of_indices(uint32_t x) {
          (static_cast<uint32_t>(__popc(x & 0xFFFF0000u) & 1) << 4);
 }
 
-// Syndrome of segment (off, n) of the packet stream `w`: positions 1..n are
-// stream bits off .. off+n-1.  Warp-collective; every lane returns s.
+// The decode buffer holds the packet from bit kPadBits on (one zero-padded
+// 16-byte slot in front), so position 0 of the first segment -- stream bit -1
+// -- is still inside the buffer and every chunk is one funnel shift.
+constexpr uint32_t kPadBits = 128;
+
+// Syndrome of segment (off, n): positions 1..n are stream bits off .. off+n-1.
+// Chunk j = positions 32j .. 32j+31 = buffer bits off + kPadBits - 1 + 32j:
+// a constant shift for every chunk.  Warp-collective; every lane returns s.
 __device__ __forceinline__ uint32_t segment_syndrome(const uint32_t* w, uint32_t off, uint32_t n, int lane) {
   const uint32_t chunks = (n + 32) / 32;  // positions 0..n
+  const uint32_t o = off + kPadBits - 1;
+  const uint32_t qb = o >> 5, rb = o & 31u;
   uint32_t X = 0, P = 0;
   for (uint32_t j = lane; j < chunks; j += 32) {
-    // chunk j = positions 32j .. 32j+31 = stream bits off + 32j - 1 ...
-    uint32_t x;
-    if (j == 0) x = (off == 0 ? (w[0] << 1) : sm_bits32(w, off - 1)) & ~1u;  // position 0 is not a position
-    else x = sm_bits32(w, off + 32 * j - 1);
-    const uint32_t last = n - 32 * j;  // highest position index inside this chunk, if < 32
-    if (last < 31) x &= low_mask(last + 1);
+    uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb);
+    const uint32_t last = n - 32 * j;  // highest position index inside this chunk
+    x &= (last < 31 ? low_mask(last + 1) : 0xFFFFFFFFu) & (j == 0 ? 0xFFFFFFFEu : 0xFFFFFFFFu);
     X ^= x;
     P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
   }
@@ -125,14 +129,14 @@ __device__ __forceinline__ uint32_t segment_msg_word(const uint32_t* w, uint32_t
   uint32_t j = run_of(d);
   uint32_t run_end = (2u << j) - j - 2;  // first data index of the next run
   if (b1 - moff <= run_end) {            // one run: one funnel-shifted slice
-    const uint32_t x = sm_bits32(w, off + d + j + 1);
+    const uint32_t x = sm_bits32(w, off + kPadBits + d + j + 1);
     return (b1 - b0 == 32u) ? x : ((x & low_mask(b1 - b0)) << (b0 - 32u * mw));
   }
   uint32_t out = 0;
   uint32_t b = b0;
   while (b < b1) {
     const uint32_t take = min(b1, moff + run_end) - b;
-    out |= (sm_bits32(w, off + d + j + 1) & low_mask(take)) << (b - 32u * mw);
+    out |= (sm_bits32(w, off + kPadBits + d + j + 1) & low_mask(take)) << (b - 32u * mw);
     b += take;
     d += take;
     ++j;
@@ -162,20 +166,21 @@ __device__ __forceinline__ uint32_t segment_code_word(const uint32_t* msg, uint3
   return out;
 }
 
-// Decode the packet held in shared memory `w` into the shared message buffer
-// `mbuf` (zeroed here); returns (per lane 0) the packet status and writes
-// syndromes.  Warp-collective.
+// Decode the packet held in shared memory `w` (from bit kPadBits on) into the
+// shared message buffer `mbuf`; returns the packet status and writes the
+// syndromes.  Words strictly inside a segment's last run -- most of them --
+// are one funnel shift with a per-segment constant offset; the rest take the
+// general run walk.  Only a segment's first message word can already hold
+// the previous segment's bits, so it alone is OR-ed.  Warp-collective.
 __device__ __forceinline__ uint32_t decode_packet_warp(const PacketGeom& g, uint32_t* w, uint32_t* mbuf, int lane,
                                                        uint16_t* syn_out, uint32_t& n_corr, uint32_t& n_fail) {
-  const uint32_t mwords = (g.msg_bytes + 3) / 4;
-  for (uint32_t i = lane; i < mwords; i += 32) mbuf[i] = 0;
   uint32_t status = 0;
   for (uint32_t i = 0; i < g.t; ++i) {
-    const uint32_t off = g.off[i], n = g.n[i], k = g.k[i], moff = g.moff[i];
+    const uint32_t off = g.off[i], n = g.n[i], k = g.k[i], moff = g.moff[i], r = g.r[i];
     const uint32_t s = segment_syndrome(w, off, n, lane);
-    if (s != 0 && s <= n) {  // EC: flip position s (stream bit off + s - 1)
+    if (s != 0 && s <= n) {  // EC: flip position s
       if (lane == 0) {
-        const uint32_t b = off + s - 1;
+        const uint32_t b = off + kPadBits + s - 1;
         w[b >> 5] ^= 1u << (b & 31);
       }
       status = max(status, 1u);
@@ -186,9 +191,20 @@ __device__ __forceinline__ uint32_t decode_packet_warp(const PacketGeom& g, uint
     }
     __syncwarp();
     if (syn_out != nullptr && lane == 0) syn_out[i] = static_cast<uint16_t>(s);
-    // RR + merger: message words touched by this segment
+    // RR + merger
+    const uint32_t J = r - 1;                                    // last run
+    const uint32_t last_lo = moff + (1u << J) - J - 1;           // first message bit of the last run
+    const uint32_t fast_lo = (last_lo + 31) / 32, fast_hi = (moff + k) / 32;  // whole words inside it
+    const uint32_t C = off + kPadBits + J + 1 - moff;            // buffer bit = message bit + C
+    const uint32_t cq = C >> 5, cr = C & 31u;
     const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
-    for (uint32_t mw = mw0 + lane; mw < mw1; mw += 32) mbuf[mw] |= segment_msg_word(w, off, k, moff, mw);
+    for (uint32_t mw = mw0 + lane; mw < mw1; mw += 32) {
+      uint32_t v;
+      if (mw >= fast_lo && mw < fast_hi && r >= 2) v = __funnelshift_r(w[mw + cq], w[mw + cq + 1], cr);
+      else v = segment_msg_word(w, off, k, moff, mw);
+      if (mw == mw0 && (moff & 31u)) mbuf[mw] |= v;
+      else mbuf[mw] = v;
+    }
     __syncwarp();
   }
   return status;
@@ -265,22 +281,48 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     packets_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ PacketArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_counts[2];
+  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* wb = smem + warp * (g.in_cap + g.msg_cap);
-  uint32_t* w = reinterpret_cast<uint32_t*>(wb);                 // packet stream
-  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + g.in_cap);   // message
+  constexpr uint32_t kBufs = (MODE == kPktDecode) ? 2 : 1;
+  uint8_t* wb = smem + warp * (kBufs * g.in_cap + g.msg_cap);
+  uint32_t* w = reinterpret_cast<uint32_t*>(wb);                          // packet stream (encode/generate)
+  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kBufs * g.in_cap);    // message
+  uint64_t* bars = bars_all + warp * 2;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  const uint64_t pol = policy_evict_first();
   uint32_t n_corr = 0, n_fail = 0;
-  for (uint64_t pk = gw; pk < a.n_packets; pk += nw) {
+  if constexpr (MODE == kPktDecode) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
+      for (uint32_t b = 0; b < 2; ++b) {
+        const uint64_t pk = gw + b * nw;
+        if (pk < a.n_packets) {
+          mbar_arrive_expect_tx(&bars[b], g.in_bytes);
+          bulk_g2s(wb + b * g.in_cap + 16, a.in + pk * a.in_stride, g.in_bytes, &bars[b], pol);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  uint32_t it = 0;
+  for (uint64_t pk = gw; pk < a.n_packets; pk += nw, ++it) {
     if constexpr (MODE == kPktDecode) {
-      const uint4* src = reinterpret_cast<const uint4*>(a.in + pk * a.in_stride);
-      for (uint32_t i = lane; i < g.in_bytes / 16; i += 32) reinterpret_cast<uint4*>(w)[i] = src[i];
-      if (lane < 4) w[g.in_bytes / 4 + lane] = 0;
-      __syncwarp();
-      const uint32_t st = decode_packet_warp(g, w, mbuf, lane, a.syn ? a.syn + pk * g.t : nullptr, n_corr, n_fail);
+      const uint32_t buf = it & 1u;
+      uint32_t* wcur = reinterpret_cast<uint32_t*>(wb + buf * g.in_cap);
+      mbar_wait(&bars[buf], (it >> 1) & 1u);
+      const uint32_t st = decode_packet_warp(g, wcur, mbuf, lane, a.syn ? a.syn + pk * g.t : nullptr, n_corr, n_fail);
+      if (lane == 0) {  // the buffer is consumed: prefetch the packet two steps ahead into it
+        const uint64_t nx = pk + 2 * nw;
+        if (nx < a.n_packets) {
+          mbar_arrive_expect_tx(&bars[buf], g.in_bytes);
+          bulk_g2s(reinterpret_cast<uint8_t*>(wcur) + 16, a.in + nx * a.in_stride, g.in_bytes, &bars[buf], pol);
+        }
+      }
       if (a.status != nullptr && lane == 0) a.status[pk] = static_cast<uint8_t>(st);
       uint8_t* dst = a.out + pk * a.out_stride;
       if (((reinterpret_cast<uintptr_t>(a.out) | a.out_stride | g.msg_bytes) & 15u) == 0) {
@@ -350,7 +392,7 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const size_t smem = static_cast<size_t>(kPktWarps) * (g.in_cap + g.msg_cap);
+  const size_t smem = static_cast<size_t>(kPktWarps) * ((MODE == kPktDecode ? 2 : 1) * g.in_cap + g.msg_cap);
   auto kfn = packets_kernel<MODE>;
   e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets)");

@@ -153,3 +153,32 @@ def test_packet_generator(oracle):
     out, syn, st = oracle.decode_packets(M, t, z, 20, stride)
     assert np.array_equal(out, msg0) and (st == 0).all() and not syn.any()
     assert np.array_equal(msg0, msg)     # the error draws do not change the messages
+
+
+def test_decode_packet_uncorrectable_path(oracle):
+    """A segment whose syndrome names no position (s > n) makes the
+    packet status 2, reports s, and leaves that segment as received (R15)."""
+    M, t = 1, 1
+    k, n, _ = oracle.packet_layout(8, 1)
+    assert n == [12]
+    msg = np.array([0xA7], np.uint8)
+    bits = np.unpackbits(oracle.encode_packet(M, t, msg), bitorder="little")
+    bits[12 - 1] ^= 1
+    bits[1 - 1] ^= 1          # s = 12 ^ 1 = 13 > n = 12
+    rx = np.packbits(bits, bitorder="little")
+    out, syn, st = oracle.decode_packet(M, t, rx)
+    assert int(syn[0]) == 13 and st == 2
+    # as received: position 12 (data bit 7) flipped, position 1 is parity
+    assert int(out[0]) == 0xA7 ^ 0x80
+    # two segments: the clean one is still decoded, the packet still fails
+    M, t = 4, 2
+    k, n, _ = oracle.packet_layout(32, 2)
+    msg = np.array([1, 2, 3, 4], np.uint8)
+    bits = np.unpackbits(oracle.encode_packet(M, t, msg), bitorder="little")
+    off = n[0]
+    bits[off + 3 - 1] ^= 1
+    bits[off + n[1] - 1] ^= 1   # s = 3 ^ n1
+    s_exp = 3 ^ n[1]
+    out, syn, st = oracle.decode_packet(M, t, np.packbits(bits, bitorder="little"))
+    assert int(syn[0]) == 0 and int(syn[1]) == s_exp
+    assert st == (2 if s_exp > n[1] else 1)
