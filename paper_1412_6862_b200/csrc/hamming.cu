@@ -625,7 +625,7 @@ template <class Op, int WARPS, int STAGES, bool INPLACE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
                  uint64_t n_full, uint32_t rem, uint64_t in_total, uint64_t out_total,
-                 unsigned long long* __restrict__ counter, typename Op::Args args) {
+                 unsigned long long* __restrict__ counter, int store_count, typename Op::Args args) {
   using TL = TileLayout<Op, INPLACE>;
   constexpr int IN = TL::IN, OUT = TL::OUT;
   constexpr int WARP_SMEM = TL::warp_bytes(STAGES);
@@ -728,7 +728,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncthreads();
     if (lane == 0 && cnt) atomicAdd(&block_cnt, static_cast<unsigned long long>(cnt));
     __syncthreads();
-    if (threadIdx.x == 0 && block_cnt) atomicAdd(counter, block_cnt);
+    if (threadIdx.x == 0) {
+      if (store_count) *counter = block_cnt;  // a single-CTA launch owns the count: no memset needed
+      else if (block_cnt) atomicAdd(counter, block_cnt);
+    }
   }
 }
 
@@ -789,16 +792,20 @@ struct Launcher {
     const uint64_t n_full = n_cw / kTileCw;
     const uint32_t rem = static_cast<uint32_t>(n_cw - n_full * kTileCw);
     int launches = 0;
-    if (counter != nullptr && !accumulate) {  // the count is overwritten, stream-ordered
-      e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
-    }
     int grid = 0;
     const uint64_t n_tiles = n_full + (rem > 0 ? 1 : 0);
     if (n_tiles > 0) {
       const uint64_t want = (n_tiles + WARPS - 1) / WARPS;
       grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * bps));
-      kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_full, rem, in_total, out_total, counter, args);
+    }
+    const int store_count = (counter != nullptr && !accumulate && grid == 1) ? 1 : 0;
+    if (counter != nullptr && !accumulate && !store_count) {  // the count is overwritten, stream-ordered
+      e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+    }
+    if (grid > 0) {
+      kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_full, rem, in_total, out_total, counter,
+                                              store_count, args);
       ++launches;
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e, "tiles kernel launch");
@@ -877,6 +884,9 @@ bool bits_overflow(int m, uint64_t N) {
 #define HAM_IP6 true
 #endif
 
+// Below this many codewords a call uses the light small-packet launch.
+constexpr uint64_t kSmallPacketCw = 1u << 16;
+
 // One-time per-device build of the (15,11) table in global memory.
 std::once_flag g_lut15_once[kMaxDev];
 cudaError_t g_lut15_err[kMaxDev];
@@ -902,6 +912,21 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
                                unsigned long long* counter, cudaStream_t st, bool accumulate) {
   const uint64_t n = (1ull << m) - 1, k = n - m;
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
+  if (N < kSmallPacketCw) {
+    // Small packets are latency-bound: a light CTA (4 warps, 2 stages, no
+    // table to build or copy) launches and finishes fastest.
+    switch (m) {
+#define HAMMING_SMALL_CASE(MM) \
+  case MM:                     \
+    return Launcher<DecodeOp<MM>, 4, 2, true>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+      HAMMING_SMALL_CASE(2)
+      HAMMING_SMALL_CASE(3)
+      HAMMING_SMALL_CASE(4)
+      HAMMING_SMALL_CASE(5)
+      HAMMING_SMALL_CASE(6)
+#undef HAMMING_SMALL_CASE
+    }
+  }
   switch (m) {
     case 2:
       return Launcher<DecodeOp<2>, HAM_W2, HAM_S2, HAM_IP2>::run(in, out, syn, N, ib, ob, counter, {}, st,
