@@ -132,6 +132,33 @@ hamming_status hamming_decode_host(int m, const void *rx_host, uint64_t n_codewo
                                    void *workspace_dev, uint64_t chunk_codewords,
                                    int n_streams);
 
+/* ------------------------------------------- SECDED: extended Hamming (f4) */
+
+/* Extended Hamming / SECDED codes (2^m, 2^m-1-m), m in [3, 6] -- (8,4),
+ * (16,11), (32,26), (64,57) -- SURVEY.md 8(f) f4, reading R17:
+ * codeword c = stream bits [c 2^m, (c+1) 2^m); its bit 0 is the overall
+ * (even) parity of all 2^m bits and bits 1..n (positions 1..n) are the
+ * Hamming codeword of hamming_decode.  Decoding: s = syndrome over positions
+ * 1..n, P = parity of all 2^m bits;
+ *   P = 1: single error at position s (s = 0: the parity bit) -- corrected;
+ *   P = 0, s != 0: double error DETECTED -- nothing is changed;
+ *   P = 0, s = 0: clean.
+ * flags_dev (N bytes or NULL): s | 0x40 if corrected | 0x80 if detected.
+ * counts_dev: 2 device uint64, OVERWRITTEN with {corrected, detected}.
+ * data_dev: as hamming_decode (k bits per codeword, pad bits 0).  Buffers
+ * 16-byte aligned, non-overlapping. */
+uint64_t hamming_secded_coded_bytes(int m, uint64_t n_codewords); /* N 2^m / 8; 0 on bad m */
+hamming_status hamming_decode_secded(int m, const void *rx_dev, uint64_t n_codewords, void *data_dev,
+                                     uint8_t *flags_dev, unsigned long long *counts_dev, void *stream);
+hamming_status hamming_encode_secded(int m, const void *data_dev, uint64_t n_codewords, void *rx_dev,
+                                     void *stream);
+/* Seeded SECDED channel: the draws of hamming_channel_generate, flip positions
+ * drawn over all 2^m bits: b1 = umulhi(lo32(u(g,3)), 2^m), b2 = (b1 + 1 +
+ * umulhi(hi32(u(g,3)), 2^m - 1)) mod 2^m (bit index, 0 = the parity bit). */
+hamming_status hamming_channel_generate_secded(int m, uint64_t seed, uint64_t c_first, uint64_t n_codewords,
+                                               uint64_t thresh, int all, uint64_t q2thresh, void *rx_dev,
+                                               void *stream);
+
 /* ------------------------------------- packets: the paper's workload (f2) */
 
 /* The paper's packets (Fig. 1): a message of msg_bytes bytes

@@ -67,6 +67,11 @@ def lib() -> ctypes.CDLL:
                                            ctypes.c_void_p]
         L.oracle_generate_packets.argtypes = [ctypes.c_uint32, ctypes.c_int, u64, u64, u64, u64, ctypes.c_int,
                                               ctypes.c_void_p, u64, ctypes.c_void_p]
+        L.oracle_decode_secded.argtypes = [ctypes.c_int, ctypes.c_void_p, u64, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.oracle_encode_secded.argtypes = [ctypes.c_int, ctypes.c_void_p, u64, ctypes.c_void_p]
+        L.oracle_generate_secded.argtypes = [ctypes.c_int, u64, u64, u64, u64, ctypes.c_int, u64,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -309,3 +314,41 @@ def decode_packets(msg_bytes: int, t: int, rx: np.ndarray, count: int, stride: i
     with ThreadPoolExecutor(max(1, threads)) as ex:
         list(ex.map(run, _ranges(count, threads, align=1)))
     return msg, syn, status
+
+
+# ------------------------------------------------------- SECDED (extended Hamming)
+def secded_coded_bytes(m: int, count: int) -> int:
+    return (count << m) // 8
+
+
+def decode_secded(m: int, rx: np.ndarray, count: int):
+    """Returns (data, flags[count] = s | 0x40 corrected | 0x80 double detected,
+    corrected, detected)."""
+    rx = np.ascontiguousarray(rx, dtype=np.uint8)
+    data = np.full(data_bytes(m, count), 0xFF, np.uint8)
+    flags = np.full(count, 0xFF, np.uint8)
+    c1, c2 = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    if lib().oracle_decode_secded(m, _ptr(rx), count, _ptr(data), _ptr(flags), ctypes.byref(c1),
+                                  ctypes.byref(c2)) != 0:
+        raise RuntimeError("oracle_decode_secded failed")
+    return data, flags, int(c1.value), int(c2.value)
+
+
+def encode_secded(m: int, data: np.ndarray, count: int) -> np.ndarray:
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    rx = np.zeros(secded_coded_bytes(m, count), np.uint8)
+    if lib().oracle_encode_secded(m, _ptr(data), count, _ptr(rx)) != 0:
+        raise RuntimeError("oracle_encode_secded failed")
+    return rx
+
+
+def generate_secded(m: int, seed: int, c_first: int, count: int, p: float = 0.1, q2: float = 0.0,
+                    want_sent: bool = False, want_err: bool = False):
+    thresh, all_, q2t = channel_thresholds(p, q2)
+    rx = np.zeros(secded_coded_bytes(m, count), np.uint8)
+    sent = np.zeros(data_bytes(m, count), np.uint8) if want_sent else None
+    err = np.zeros(2 * count, np.uint8) if want_err else None
+    if lib().oracle_generate_secded(m, seed & (2 ** 64 - 1), c_first, count, thresh, all_, q2t, _ptr(rx),
+                                    _ptr(sent), _ptr(err)) != 0:
+        raise RuntimeError("oracle_generate_secded failed")
+    return rx, sent, err

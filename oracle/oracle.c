@@ -483,3 +483,120 @@ int oracle_generate_packets(uint32_t msg_bytes, int t, uint64_t seed, uint64_t g
     }
     return 0;
 }
+
+/* ================================================================== */
+/* Extended Hamming / SECDED (reading R17): a   */
+/* codeword of 2^m bits whose bit 0 (position 0) is the overall parity */
+/* over all 2^m bits (even) and whose positions 1..n, n = 2^m - 1, are */
+/* the Hamming codeword.  Codeword c = stream bits [c 2^m, (c+1) 2^m). */
+/* ================================================================== */
+
+/* Decode: s = syndrome over positions 1..n (index sets, as above);
+ * P = XOR of all 2^m bits.
+ *   P = 1: one error -- at position s (s = 0: the parity bit itself) --
+ *          corrected; flags bit 6.
+ *   P = 0, s != 0: two errors detected, nothing corrected; flags bit 7.
+ *   P = 0, s = 0: clean.
+ * flags[c] = s | bit6 | bit7 (nullable); data as in oracle_decode;
+ * *corrected / *detected count the two cases. */
+int oracle_decode_secded(int m, const uint8_t *rx, uint64_t count, uint8_t *data_out, uint8_t *flags,
+                         uint64_t *corrected, uint64_t *detected)
+{
+    if (m < 3 || m > 6) return -1;
+    int n = code_n(m);
+    int k = n - m;
+    int w = n + 1;
+    uint8_t bits[64];
+    uint8_t msg[64];
+    uint64_t fixed = 0, found = 0;
+    for (uint64_t c = 0; c < count; c++) {
+        for (int b = 0; b < w; b++) bits[b] = (uint8_t)get_bit(rx, c * (uint64_t)w + (uint64_t)b);
+        int s = oracle_syndrome_bits(n, bits + 1);          /* positions 1..n */
+        int P = 0;
+        for (int b = 0; b < w; b++) P = P ^ bits[b];
+        int f = 0;
+        if (P == 1) {
+            bits[s] ^= 1;                                    /* position s (0 = the parity bit) */
+            f = 0x40;
+            fixed++;
+        } else if (s != 0) {
+            f = 0x80;
+            found++;
+        }
+        oracle_remove_redundancy_bits(n, bits + 1, msg);
+        for (int i = 0; i < k; i++) put_bit(data_out, c * (uint64_t)k + (uint64_t)i, msg[i]);
+        if (flags) flags[c] = (uint8_t)(s | f);
+    }
+    uint64_t total = count * (uint64_t)k;
+    for (uint64_t b = total; b < ((total + 7) / 8) * 8; b++) put_bit(data_out, b, 0);
+    if (corrected) *corrected = fixed;
+    if (detected) *detected = found;
+    return 0;
+}
+
+/* Encode: Hamming-encode positions 1..n, then bit 0 = XOR of positions 1..n. */
+int oracle_encode_secded(int m, const uint8_t *data, uint64_t count, uint8_t *rx)
+{
+    if (m < 3 || m > 6) return -1;
+    int n = code_n(m);
+    int k = n - m;
+    int w = n + 1;
+    uint8_t msg[64], cw[64];
+    for (uint64_t c = 0; c < count; c++) {
+        for (int i = 0; i < k; i++) msg[i] = (uint8_t)get_bit(data, c * (uint64_t)k + (uint64_t)i);
+        oracle_encode_bits(n, msg, cw + 1);
+        int P = 0;
+        for (int p = 1; p <= n; p++) P = P ^ cw[p];
+        cw[0] = (uint8_t)P;
+        for (int b = 0; b < w; b++) put_bit(rx, c * (uint64_t)w + (uint64_t)b, cw[b]);
+    }
+    return 0;
+}
+
+/* Seeded SECDED channel: the draws of oracle_generate, positions drawn over
+ * all 2^m bits (bit index 0 = the parity bit):
+ *   b1 = umulhi(lo32(u(g,3)), 2^m), b2 = (b1 + 1 + umulhi(hi32(u(g,3)), 2^m - 1)) mod 2^m;
+ * err (nullable) records b1 + 1, b2 + 1 (0 = no flip). */
+int oracle_generate_secded(int m, uint64_t seed, uint64_t c_first, uint64_t count,
+                           uint64_t thresh, int all, uint64_t q2thresh,
+                           uint8_t *rx, uint8_t *sent, uint8_t *err)
+{
+    if (m < 3 || m > 6) return -1;
+    int n = code_n(m);
+    int k = n - m;
+    int w = n + 1;
+    uint8_t msg[64], cw[64];
+    for (uint64_t i = 0; i < count; i++) {
+        uint64_t c = c_first + i;
+        uint64_t u0 = draw(seed, c, 0);
+        uint64_t u1 = draw(seed, c, 1);
+        uint64_t u2 = draw(seed, c, 2);
+        uint64_t u3 = draw(seed, c, 3);
+        for (int b = 0; b < k; b++) msg[b] = (uint8_t)((u0 >> b) & 1);
+        oracle_encode_bits(n, msg, cw + 1);
+        int P = 0;
+        for (int p = 1; p <= n; p++) P = P ^ cw[p];
+        cw[0] = (uint8_t)P;
+        int b1 = -1, b2 = -1;
+        if (all || u1 < thresh) {
+            b1 = (int)(((u3 & 0xFFFFFFFFULL) * (uint64_t)w) >> 32);
+            cw[b1] ^= 1;
+            if ((u2 >> 32) < q2thresh) {
+                b2 = (int)(((uint64_t)b1 + 1 + (((u3 >> 32) * (uint64_t)(w - 1)) >> 32)) % (uint64_t)w);
+                cw[b2] ^= 1;
+            }
+        }
+        for (int b = 0; b < w; b++) put_bit(rx, i * (uint64_t)w + (uint64_t)b, cw[b]);
+        if (sent)
+            for (int b = 0; b < k; b++) put_bit(sent, i * (uint64_t)k + (uint64_t)b, msg[b]);
+        if (err) {
+            err[2 * i] = (uint8_t)(b1 + 1);
+            err[2 * i + 1] = (uint8_t)(b2 + 1);
+        }
+    }
+    if (sent) {
+        uint64_t tk = count * (uint64_t)k;
+        for (uint64_t b = tk; b < ((tk + 7) / 8) * 8; b++) put_bit(sent, b, 0);
+    }
+    return 0;
+}

@@ -61,6 +61,14 @@ def lib() -> ctypes.CDLL:
     L.hamming_decode_host.argtypes = [c_int, vp, u64, vp, vp, vp, vp, u64, c_int]
     L.hamming_decode_host.restype = c_int
     u32 = ctypes.c_uint32
+    L.hamming_secded_coded_bytes.argtypes = [c_int, u64]
+    L.hamming_secded_coded_bytes.restype = u64
+    L.hamming_decode_secded.argtypes = [c_int, vp, u64, vp, vp, vp, vp]
+    L.hamming_decode_secded.restype = c_int
+    L.hamming_encode_secded.argtypes = [c_int, vp, u64, vp, vp]
+    L.hamming_encode_secded.restype = c_int
+    L.hamming_channel_generate_secded.argtypes = [c_int, u64, u64, u64, u64, c_int, u64, vp, vp]
+    L.hamming_channel_generate_secded.restype = c_int
     L.hamming_packet_coded_bytes.argtypes = [u32, c_int]
     L.hamming_packet_coded_bytes.restype = u64
     L.hamming_packet_layout.argtypes = [u32, c_int, vp, vp]

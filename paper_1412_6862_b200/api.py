@@ -264,3 +264,75 @@ def hamming_packet_channel_generate(msg_bytes: int, t: int, seed: int, g_first: 
 
 
 packet_channel_generate = hamming_packet_channel_generate
+
+
+# ------------------------------------------------------- SECDED (extended Hamming)
+def secded_coded_bytes(m: int, n_codewords: int) -> int:
+    v = int(lib().hamming_secded_coded_bytes(m, n_codewords))
+    if n_codewords and v == 0:
+        raise ValueError("SECDED needs m in [3, 6]")
+    return v
+
+
+@dataclass
+class SecdedResult:
+    data: torch.Tensor             # uint8 [data_bytes(m, N)]
+    flags: Optional[torch.Tensor]  # uint8 [N]: s | 0x40 corrected | 0x80 double error detected
+    counts: torch.Tensor           # int64 [2]: corrected, detected
+
+
+def hamming_decode_secded(m: int, rx: torch.Tensor, n_codewords: int, *, data_out: Optional[torch.Tensor] = None,
+                          flags: bool | torch.Tensor = True, counts: Optional[torch.Tensor] = None,
+                          stream: Optional[torch.cuda.Stream] = None) -> SecdedResult:
+    N = int(n_codewords)
+    dev = rx.device
+    if data_out is None:
+        data_out = torch.empty(max(1, data_bytes(m, N)), dtype=torch.uint8, device=dev)
+    if flags is True:
+        fl = torch.empty(max(1, N), dtype=torch.uint8, device=dev)
+    elif flags is False or flags is None:
+        fl = None
+    else:
+        fl = flags
+    if counts is None:
+        counts = torch.empty(2, dtype=torch.int64, device=dev)
+    st = lib().hamming_decode_secded(m, _dev_ptr(rx, "rx", secded_coded_bytes(m, N)), N,
+                                     _dev_ptr(data_out, "data_out", data_bytes(m, N)), _dev_ptr(fl, "flags", N),
+                                     _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
+    check(st, "hamming_decode_secded")
+    return SecdedResult(data_out, fl, counts)
+
+
+decode_secded = hamming_decode_secded
+
+
+def hamming_encode_secded(m: int, data: torch.Tensor, n_codewords: int, *, rx_out: Optional[torch.Tensor] = None,
+                          stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    N = int(n_codewords)
+    if rx_out is None:
+        rx_out = torch.empty(max(1, secded_coded_bytes(m, N)), dtype=torch.uint8, device=data.device)
+    st = lib().hamming_encode_secded(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
+                                     _dev_ptr(rx_out, "rx_out", secded_coded_bytes(m, N)),
+                                     _stream_handle(stream, data.device))
+    check(st, "hamming_encode_secded")
+    return rx_out
+
+
+encode_secded = hamming_encode_secded
+
+
+def hamming_channel_generate_secded(m: int, seed: int, c_first: int, n_codewords: int, p: float = 0.1,
+                                    q2: float = 0.0, *, device=None,
+                                    stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    N = int(n_codewords)
+    thresh, all_, q2t = channel_thresholds(p, q2)
+    rx = torch.empty(max(1, secded_coded_bytes(m, N)), dtype=torch.uint8,
+                     device=device if device is not None else "cuda")
+    st = lib().hamming_channel_generate_secded(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
+                                               _dev_ptr(rx, "rx", secded_coded_bytes(m, N)),
+                                               _stream_handle(stream, rx.device))
+    check(st, "hamming_channel_generate_secded")
+    return rx
+
+
+channel_generate_secded = hamming_channel_generate_secded

@@ -168,6 +168,15 @@ __device__ __forceinline__ void put_field(uint32_t (&o)[NO], int b, uint32_t src
   if (r + len > 32) o[q + 1] |= (src >> (pos + 32 - r)) & (m >> (32 - r));
 }
 
+// Count of nonzero syndrome bytes in the lane's 8 side words (s <= 63, so
+// adding 0x7F to a byte never carries into the next one).
+__device__ __forceinline__ uint32_t count_nonzero_bytes(const uint32_t (&w)[8]) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += ((w[i] + 0x7F7F7F7Fu) & 0x80808080u) >> 7;
+  return (acc * 0x01010101u) >> 24;  // four byte lanes of at most 8 each
+}
+
 // --------------------------------------------------------- per-codeword math
 // Decode one codeword given as v = (lo, hi): bit p of v holds position p
 // (hi bit i = position 32 + i; hi unused for m <= 5).  Returns the syndrome s
@@ -268,23 +277,48 @@ __device__ __forceinline__ void put_codeword(uint32_t (&o)[NO], int b, uint32_t 
 // `side` = 8 words of per-codeword bytes (syndromes).
 // `valid` = number of the lane's 32 codewords that exist (32 except in the tail).
 
-template <int M>
+// EXT = false: the perfect (2^m-1, 2^m-1-m) code, codeword c = lane-stream
+// bits [c n, c n + n).  EXT = true: extended Hamming / SECDED (SURVEY.md 8(f)
+// f4, reading R17), codeword c = bits [c 2^m, (c+1) 2^m) with bit 0 the
+// overall parity -- register bit p is position p in both cases (bit 0 is the
+// dummy resp. the parity bit), so a2..a5 are shared.
+template <int M, bool EXT = false>
 struct DecodeOp {
-  static constexpr int IN_W = Geo<M>::n;
+  static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
+  static constexpr int IN_W = CW_BITS;  // 32 codewords of a lane
   static constexpr int OUT_W = Geo<M>::k;
-  static constexpr int IN_BITS = Geo<M>::n;  // per codeword
+  static constexpr int IN_BITS = CW_BITS;  // per codeword
   static constexpr bool HAS_SIDE = true;
+  static constexpr int NCOUNT = EXT ? 2 : 1;
   static constexpr int SHARED = 0;  // CTA-shared bytes (lookup tables)
   struct Args {};
   __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
+  // counts from the side bytes: perfect code -- nonzero syndromes; SECDED --
+  // [corrected (bit 6), double errors detected (bit 7)]
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) {
+    if constexpr (EXT) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c += __popc(sw[i] & 0x40404040u);
+      return c;
+    } else {
+      return count_nonzero_bytes(sw);
+    }
+  }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&sw)[8]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += __popc(sw[i] & 0x80808080u);
+    return c;
+  }
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                   uint32_t (&side)[8], uint64_t /*cw0*/, int /*valid*/,
                                                   const Args&, const uint8_t* /*sh*/) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
-    uint32_t w[n];
+    uint32_t w[IN_W];
 #pragma unroll
-    for (int i = 0; i < n; ++i) w[i] = in[i];
+    for (int i = 0; i < IN_W; ++i) w[i] = in[i];
     __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     uint32_t o[k];
 #pragma unroll
@@ -292,18 +326,35 @@ struct DecodeOp {
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       uint32_t lo, hi = 0;
-      if (c == 0) {  // v = w << 1 (no previous codeword: dummy bit 0 = 0)
+      if constexpr (EXT) {  // word-aligned 2^m-bit codewords
+        if constexpr (M == 6) {
+          lo = w[2 * c];
+          hi = w[2 * c + 1];
+        } else {
+          lo = take_bits(w, c * CW_BITS);
+        }
+      } else if (c == 0) {  // v = w << 1 (no previous codeword: dummy bit 0 = 0)
         lo = w[0] << 1;
         if constexpr (M == 6) hi = __funnelshift_l(w[0], w[1], 1);
-      } else {       // v = lane-stream bits [c*n - 1, c*n - 1 + 32*(1 or 2))
+      } else {  // v = lane-stream bits [c*n - 1, c*n - 1 + 32*(1 or 2))
         lo = take_bits(w, c * n - 1);
         if constexpr (M == 6) hi = take_bits(w, c * n + 31);
       }
-      const uint32_t s = syndrome_cw<M>(lo, hi);                    // a2
-      if constexpr (M <= 5) {                                       // a3
-        lo ^= 1u << s;
+      const uint32_t s = syndrome_cw<M>(lo, hi);  // a2
+      uint32_t flag = 0;
+      bool flip = true;
+      if constexpr (EXT) {  // overall parity P decides: P = 1 correct, P = 0 and s != 0 detect
+        uint32_t par;
+        if constexpr (M == 6) par = __popc(lo ^ hi) & 1u;
+        else if constexpr (M == 5) par = __popc(lo) & 1u;
+        else par = __popc(lo & ((1u << CW_BITS) - 1u)) & 1u;
+        flip = par != 0;
+        flag = (par << 6) | ((par == 0 && s != 0) ? 0x80u : 0u);
+      }
+      if constexpr (M <= 5) {  // a3 (s = 0 flips bit 0: the dummy or the parity bit)
+        lo ^= flip ? (1u << s) : 0u;
       } else {
-        const uint64_t f = 1ull << s;
+        const uint64_t f = flip ? (1ull << s) : 0ull;
         lo ^= static_cast<uint32_t>(f);
         hi ^= static_cast<uint32_t>(f >> 32);
       }
@@ -313,7 +364,7 @@ struct DecodeOp {
       for (int g = 1; g < (M <= 5 ? M : 5); ++g)
         put_field(o, c * k + (1 << g) - g - 1, lo, (1 << g) + 1, (1 << g) - 1);
       if constexpr (M == 6) put_field(o, c * k + 26, hi, 1, 31);
-      side[c >> 2] |= s << (8 * (c & 3));
+      side[c >> 2] |= (s | flag) << (8 * (c & 3));
     }
 #pragma unroll
     for (int i = 0; i < k; ++i) out[i] = o[i];
@@ -343,6 +394,9 @@ __device__ __forceinline__ uint32_t insert_byte1(uint32_t word, uint32_t e, int 
 // (7,4): per-lane replicated 128-entry table, entry = data (bits 0..3) |
 // syndrome << 8; lane l reads word [x][l], always its own bank (16 KB).
 struct DecodeLut3Op {
+  static constexpr int NCOUNT = 1;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
   static constexpr bool HAS_SIDE = true;
   static constexpr int SHARED = 128 * 32 * 4;
@@ -393,6 +447,9 @@ __global__ void init_lut15_kernel() {
 }
 
 struct DecodeLut4Op {
+  static constexpr int NCOUNT = 1;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 15, OUT_W = 11, IN_BITS = 15;
   static constexpr bool HAS_SIDE = true;
   static constexpr int SHARED = 32768 * 2;
@@ -430,12 +487,31 @@ struct DecodeLut4Op {
   }
 };
 
-template <int M>
+// SECDED: set bit 0 (position 0) to the parity of positions 1..n and emit the
+// whole 2^m-bit codeword at lane-stream bit b.
+template <int M, int NO>
+__device__ __forceinline__ void put_ext_codeword(uint32_t (&o)[NO], int b, uint32_t lo, uint32_t hi) {
+  if constexpr (M == 6) {
+    lo = (lo & ~1u) | (static_cast<uint32_t>(__popc((lo & ~1u) ^ hi)) & 1u);
+    o[b >> 5] = lo;
+    o[(b >> 5) + 1] = hi;
+  } else {
+    constexpr int W = 1 << M;
+    constexpr uint32_t mask = (W == 32) ? 0xFFFFFFFFu : ((1u << W) - 1u);
+    lo &= mask & ~1u;
+    lo |= static_cast<uint32_t>(__popc(lo)) & 1u;
+    put_bits(o, b, lo, W);
+  }
+}
+
+template <int M, bool EXT = false>
 struct EncodeOp {
+  static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
   static constexpr int IN_W = Geo<M>::k;
-  static constexpr int OUT_W = Geo<M>::n;
+  static constexpr int OUT_W = CW_BITS;
   static constexpr int IN_BITS = Geo<M>::k;
   static constexpr bool HAS_SIDE = false;
+  static constexpr int NCOUNT = 1;
   static constexpr int SHARED = 0;
   struct Args {};
   __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
@@ -446,9 +522,9 @@ struct EncodeOp {
     uint32_t w[k];
 #pragma unroll
     for (int i = 0; i < k; ++i) w[i] = in[i];
-    uint32_t o[n];
+    uint32_t o[OUT_W];
 #pragma unroll
-    for (int i = 0; i < n; ++i) o[i] = 0;
+    for (int i = 0; i < OUT_W; ++i) o[i] = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       uint32_t dlo, dhi = 0;
@@ -461,10 +537,12 @@ struct EncodeOp {
       }
       uint32_t lo, hi;
       encode_cw<M>(dlo, dhi, lo, hi);
-      put_codeword<M>(o, c * n, lo, hi);
+      if constexpr (EXT) put_ext_codeword<M>(o, c * CW_BITS, lo, hi);
+      else put_codeword<M>(o, c * n, lo, hi);
     }
 #pragma unroll
-    for (int i = 0; i < n; ++i) out[i] = o[i];
+    for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
+    (void)n;
   }
 };
 
@@ -476,12 +554,14 @@ __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-template <int M>
+template <int M, bool EXT = false>
 struct GenerateOp {
+  static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
   static constexpr int IN_W = 0;
-  static constexpr int OUT_W = Geo<M>::n;
+  static constexpr int OUT_W = CW_BITS;
   static constexpr int IN_BITS = 0;
   static constexpr bool HAS_SIDE = false;
+  static constexpr int NCOUNT = 1;
   static constexpr int SHARED = 0;
   struct Args {
     uint64_t seed, c_first, thresh, q2thresh;
@@ -493,9 +573,9 @@ struct GenerateOp {
                                                   uint64_t cw0, int valid, const Args& a, const uint8_t*) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
-    uint32_t o[n];
+    uint32_t o[OUT_W];
 #pragma unroll
-    for (int i = 0; i < n; ++i) o[i] = 0;
+    for (int i = 0; i < OUT_W; ++i) o[i] = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const uint64_t g = a.c_first + cw0 + c;
@@ -515,21 +595,40 @@ struct GenerateOp {
       encode_cw<M>(dlo, dhi, lo, hi);
       const bool ev = a.all || (u1 < a.thresh);
       const bool two = (u2 >> 32) < a.q2thresh;
-      const uint32_t p1 = 1u + __umulhi(static_cast<uint32_t>(u3), static_cast<uint32_t>(n));
-      uint32_t p2 = p1 + __umulhi(static_cast<uint32_t>(u3 >> 32), static_cast<uint32_t>(n - 1));  // (p1-1)+1+x
-      p2 = (p2 >= static_cast<uint32_t>(n) ? p2 - n : p2) + 1u;
-      uint64_t f = ev ? (1ull << p1) : 0ull;
-      f ^= (ev && two) ? (1ull << p2) : 0ull;
+      uint64_t f;
+      if constexpr (EXT) {  // bit indices over the whole 2^m-bit codeword (0 = the parity bit)
+        lo = (lo & ~1u) | (static_cast<uint32_t>(__popc((lo & ~1u) ^ hi)) & 1u);
+        const uint32_t b1 = __umulhi(static_cast<uint32_t>(u3), static_cast<uint32_t>(CW_BITS));
+        uint32_t b2 = b1 + 1u + __umulhi(static_cast<uint32_t>(u3 >> 32), static_cast<uint32_t>(CW_BITS - 1));
+        b2 = (b2 >= static_cast<uint32_t>(CW_BITS)) ? b2 - CW_BITS : b2;
+        f = ev ? (1ull << b1) : 0ull;
+        f ^= (ev && two) ? (1ull << b2) : 0ull;
+      } else {
+        const uint32_t p1 = 1u + __umulhi(static_cast<uint32_t>(u3), static_cast<uint32_t>(n));
+        uint32_t p2 = p1 + __umulhi(static_cast<uint32_t>(u3 >> 32), static_cast<uint32_t>(n - 1));  // (p1-1)+1+x
+        p2 = (p2 >= static_cast<uint32_t>(n) ? p2 - n : p2) + 1u;
+        f = ev ? (1ull << p1) : 0ull;
+        f ^= (ev && two) ? (1ull << p2) : 0ull;
+      }
       lo ^= static_cast<uint32_t>(f);
       hi ^= static_cast<uint32_t>(f >> 32);
       if (c >= valid) {  // past the end of the packet (tail only): emit zeros
         lo = 0;
         hi = 0;
       }
-      put_codeword<M>(o, c * n, lo, hi);
+      if constexpr (EXT) {
+        if constexpr (M == 6) {
+          o[2 * c] = lo;
+          o[2 * c + 1] = hi;
+        } else {
+          put_bits(o, c * CW_BITS, lo & ((CW_BITS == 32) ? 0xFFFFFFFFu : ((1u << CW_BITS) - 1u)), CW_BITS);
+        }
+      } else {
+        put_codeword<M>(o, c * n, lo, hi);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < n; ++i) out[i] = o[i];
+    for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
   }
 };
 // ------------------------------------------------------------------ kernels
@@ -539,15 +638,6 @@ struct TileBytes {
   static constexpr int OUT = Op::OUT_W * 128;
 };
 
-// Count of nonzero syndrome bytes in the lane's 8 side words (s <= 63, so
-// adding 0x7F to a byte never carries into the next one).
-__device__ __forceinline__ uint32_t count_nonzero_bytes(const uint32_t (&w)[8]) {
-  uint32_t acc = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc += ((w[i] + 0x7F7F7F7Fu) & 0x80808080u) >> 7;
-  return (acc * 0x01010101u) >> 24;  // four byte lanes of at most 8 each
-}
-
 // The ragged last tile (rem < 1024 codewords) of a launch: bounded 16-byte
 // loads with zero fill, input pad bits past rem codewords cleared, the same
 // lane function, bounded stores.  Runs in the warp that owns the tile.
@@ -556,7 +646,7 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
                                                uint8_t* __restrict__ side, uint64_t tile, uint32_t rem,
                                                uint64_t in_total, uint64_t out_total, uint8_t* ibuf,
                                                uint32_t* obuf, int lane, const typename Op::Args& args,
-                                               const uint8_t* sh) {
+                                               const uint8_t* sh, uint32_t& cnt2) {
   constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   if constexpr (IN > 0) {
     const uint64_t ib0 = tile * IN;
@@ -599,7 +689,8 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
       uint8_t* sp = side + tile * kTileCw + lane * 32;
       for (int c = 0; c < valid; ++c) sp[c] = static_cast<uint8_t>(sidew[c >> 2] >> (8 * (c & 3)));
     }
-    cnt = count_nonzero_bytes(sidew);  // codewords past `valid` decode zeros: s = 0
+    cnt = Op::count0(sidew);  // codewords past `valid` decode zeros: s = 0, no flags
+    if constexpr (Op::NCOUNT > 1) cnt2 += Op::count1(sidew);
   }
   return cnt;
 }
@@ -630,7 +721,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   constexpr int IN = TL::IN, OUT = TL::OUT;
   constexpr int WARP_SMEM = TL::warp_bytes(STAGES);
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ unsigned long long block_cnt;
+  __shared__ unsigned long long block_cnt[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* const sh = smem;  // Op::SHARED bytes of CTA-wide tables first
@@ -640,7 +731,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
 
-  if (threadIdx.x == 0) block_cnt = 0;
+  if (threadIdx.x < 2) block_cnt[threadIdx.x] = 0;
   if constexpr (Op::SHARED > 0) {
     Op::cta_init(sh, threadIdx.x, blockDim.x);
     __syncthreads();
@@ -662,7 +753,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
   }
 
-  uint32_t cnt = 0;
+  uint32_t cnt = 0, cnt2 = 0;
   uint32_t it = 0;
   for (uint64_t t = gw; t < n_full; t += nw, ++it) {
     const int st = static_cast<int>(it % STAGES);
@@ -711,7 +802,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         st_global_cs_v4(sp, sidew[0], sidew[1], sidew[2], sidew[3]);
         st_global_cs_v4(sp + 16, sidew[4], sidew[5], sidew[6], sidew[7]);
       }
-      cnt += count_nonzero_bytes(sidew);
+      cnt += Op::count0(sidew);
+      if constexpr (Op::NCOUNT > 1) cnt2 += Op::count1(sidew);
     }
   }
   if (rem > 0 && gw == n_full % nw) {  // the ragged tail tile
@@ -719,18 +811,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
     uint8_t* tail_out = TL::IN_PLACE ? wbase : wbase + STAGES * IN;
     cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
-                             reinterpret_cast<uint32_t*>(tail_out), lane, args, sh);
+                             reinterpret_cast<uint32_t*>(tail_out), lane, args, sh, cnt2);
   }
   if (lane == 0) bulk_wait<0>();
 
   if (counter != nullptr) {
     cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if constexpr (Op::NCOUNT > 1) cnt2 = __reduce_add_sync(0xffffffffu, cnt2);
     __syncthreads();
-    if (lane == 0 && cnt) atomicAdd(&block_cnt, static_cast<unsigned long long>(cnt));
+    if (lane == 0 && cnt) atomicAdd(&block_cnt[0], static_cast<unsigned long long>(cnt));
+    if constexpr (Op::NCOUNT > 1)
+      if (lane == 0 && cnt2) atomicAdd(&block_cnt[1], static_cast<unsigned long long>(cnt2));
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (store_count) *counter = block_cnt;  // a single-CTA launch owns the count: no memset needed
-      else if (block_cnt) atomicAdd(counter, block_cnt);
+    if (threadIdx.x < Op::NCOUNT) {
+      const unsigned long long v = block_cnt[threadIdx.x];
+      if (store_count) counter[threadIdx.x] = v;  // a single-CTA launch owns the count: no memset needed
+      else if (v) atomicAdd(&counter[threadIdx.x], v);
     }
   }
 }
@@ -800,7 +896,7 @@ struct Launcher {
     }
     const int store_count = (counter != nullptr && !accumulate && grid == 1) ? 1 : 0;
     if (counter != nullptr && !accumulate && !store_count) {  // the count is overwritten, stream-ordered
-      e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+      e = cudaMemsetAsync(counter, 0, Op::NCOUNT * sizeof(unsigned long long), stream);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
     }
     if (grid > 0) {
@@ -1156,6 +1252,107 @@ hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void*
     if (streams[i]) cudaStreamDestroy(streams[i]);
   g_launches = launches;
   return rc;
+}
+
+// ---------------------------------------------------- SECDED (extended Hamming)
+uint64_t hamming_secded_coded_bytes(int m, uint64_t N) {
+  if (m < 3 || m > 6 || N > (~0ull >> m)) return 0;
+  return (N << m) / 8;
+}
+
+hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void* data_dev, uint8_t* flags_dev,
+                                     unsigned long long* counts_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 3 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_decode_secded: m must be in [3, 6]");
+  if (N > (~0ull >> m)) return set_err(HAMMING_E_RANGE, "hamming_decode_secded: size overflows");
+  if (counts_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_decode_secded: counts is NULL");
+  if (N > 0 && (rx_dev == nullptr || data_dev == nullptr))
+    return set_err(HAMMING_E_NULL, "hamming_decode_secded: rx or data is NULL");
+  if (!aligned16(rx_dev) || !aligned16(data_dev) || !aligned16(flags_dev))
+    return set_err(HAMMING_E_MISALIGNED, "hamming_decode_secded: buffers must be 16-byte aligned");
+  const uint64_t ib = hamming_secded_coded_bytes(m, N), ob = hamming_data_bytes(m, N), sb = flags_dev ? N : 0;
+  if (ranges_overlap(rx_dev, ib, data_dev, ob) || ranges_overlap(rx_dev, ib, flags_dev, sb) ||
+      ranges_overlap(data_dev, ob, flags_dev, sb) || ranges_overlap(rx_dev, ib, counts_dev, 16) ||
+      ranges_overlap(data_dev, ob, counts_dev, 16) || ranges_overlap(flags_dev, sb, counts_dev, 16))
+    return set_err(HAMMING_E_OVERLAP, "hamming_decode_secded: buffers overlap");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint8_t* in = static_cast<const uint8_t*>(rx_dev);
+  uint8_t* out = static_cast<uint8_t*>(data_dev);
+  if (N < kSmallPacketCw) {
+    switch (m) {
+#define HAMMING_SECDED_SMALL(MM) \
+  case MM:                       \
+    return Launcher<DecodeOp<MM, true>, 4, 2, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+      HAMMING_SECDED_SMALL(3)
+      HAMMING_SECDED_SMALL(4)
+      HAMMING_SECDED_SMALL(5)
+      HAMMING_SECDED_SMALL(6)
+#undef HAMMING_SECDED_SMALL
+    }
+  }
+  switch (m) {
+    case 3: return Launcher<DecodeOp<3, true>, 16, 8, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+    case 4: return Launcher<DecodeOp<4, true>, 16, 6, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+    case 5: return Launcher<DecodeOp<5, true>, 12, 3, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+    case 6: return Launcher<DecodeOp<6, true>, 8, 3, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+  }
+  return set_err(HAMMING_E_INVALID_M, "hamming_decode_secded: m must be in [3, 6]");
+}
+
+hamming_status hamming_encode_secded(int m, const void* data_dev, uint64_t N, void* rx_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 3 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_encode_secded: m must be in [3, 6]");
+  if (N > (~0ull >> m)) return set_err(HAMMING_E_RANGE, "hamming_encode_secded: size overflows");
+  if (N == 0) return HAMMING_OK;
+  if (data_dev == nullptr || rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_encode_secded: NULL buffer");
+  if (!aligned16(data_dev) || !aligned16(rx_dev))
+    return set_err(HAMMING_E_MISALIGNED, "hamming_encode_secded: buffers must be 16-byte aligned");
+  const uint64_t ib = hamming_data_bytes(m, N), ob = hamming_secded_coded_bytes(m, N);
+  if (ranges_overlap(data_dev, ib, rx_dev, ob)) return set_err(HAMMING_E_OVERLAP, "hamming_encode_secded: overlap");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint8_t* in = static_cast<const uint8_t*>(data_dev);
+  uint8_t* out = static_cast<uint8_t*>(rx_dev);
+  switch (m) {
+#define HAMMING_SECDED_ENC(MM) \
+  case MM:                     \
+    return Launcher<EncodeOp<MM, true>, 4, 2, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    HAMMING_SECDED_ENC(3)
+    HAMMING_SECDED_ENC(4)
+    HAMMING_SECDED_ENC(5)
+    HAMMING_SECDED_ENC(6)
+#undef HAMMING_SECDED_ENC
+  }
+  return set_err(HAMMING_E_INVALID_M, "hamming_encode_secded: m must be in [3, 6]");
+}
+
+hamming_status hamming_channel_generate_secded(int m, uint64_t seed, uint64_t c_first, uint64_t N, uint64_t thresh,
+                                               int all, uint64_t q2thresh, void* rx_dev, void* stream) {
+  g_launches = 0;
+  g_grid = 0;
+  if (m < 3 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_channel_generate_secded: m must be in [3, 6]");
+  if (N > (~0ull >> m)) return set_err(HAMMING_E_RANGE, "hamming_channel_generate_secded: size overflows");
+  if (q2thresh > (1ull << 32)) return set_err(HAMMING_E_RANGE, "hamming_channel_generate_secded: q2thresh > 2^32");
+  if (N == 0) return HAMMING_OK;
+  if (rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_channel_generate_secded: rx is NULL");
+  if (!aligned16(rx_dev)) return set_err(HAMMING_E_MISALIGNED, "hamming_channel_generate_secded: rx misaligned");
+  const uint64_t ob = hamming_secded_coded_bytes(m, N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* out = static_cast<uint8_t*>(rx_dev);
+  switch (m) {
+#define HAMMING_SECDED_GEN(MM)                                                                      \
+  case MM: {                                                                                        \
+    typename GenerateOp<MM, true>::Args a{seed, c_first, thresh, q2thresh, all};                    \
+    return Launcher<GenerateOp<MM, true>, 4, 1, false>::run(nullptr, out, nullptr, N, 0, ob, nullptr, a, st); \
+  }
+    HAMMING_SECDED_GEN(3)
+    HAMMING_SECDED_GEN(4)
+    HAMMING_SECDED_GEN(5)
+    HAMMING_SECDED_GEN(6)
+#undef HAMMING_SECDED_GEN
+  }
+  return set_err(HAMMING_E_INVALID_M, "hamming_channel_generate_secded: m must be in [3, 6]");
 }
 
 // ------------------------------------------------- packets (the paper's workload)

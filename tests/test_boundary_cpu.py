@@ -138,3 +138,19 @@ def test_packet_entry_point_validation(L):
                                     None, None, None, None) == 4
     assert L.hamming_decode_packets(400, 3, ctypes.c_void_p(FAKE), stride, 4, ctypes.c_void_p(FAKE + big), 399,
                                     None, None, None, None) == 7
+
+
+def test_secded_entry_point_validation(L):
+    assert L.hamming_secded_coded_bytes(6, 1000) == 8000
+    assert L.hamming_secded_coded_bytes(3, 8) == 8
+    assert L.hamming_secded_coded_bytes(2, 8) == 0 and L.hamming_secded_coded_bytes(7, 8) == 0
+    big = 1 << 30
+    assert L.hamming_decode_secded(2, ctypes.c_void_p(FAKE), 8, ctypes.c_void_p(FAKE + big), None,
+                                   ctypes.c_void_p(FAKE + 2 * big), None) == 1
+    assert L.hamming_decode_secded(6, ctypes.c_void_p(FAKE), 8, ctypes.c_void_p(FAKE + big), None, None, None) == 2
+    assert L.hamming_decode_secded(6, ctypes.c_void_p(FAKE + 4), 8, ctypes.c_void_p(FAKE + big), None,
+                                   ctypes.c_void_p(FAKE + 2 * big), None) == 3
+    assert L.hamming_decode_secded(6, ctypes.c_void_p(FAKE), 8, ctypes.c_void_p(FAKE + 32), None,
+                                   ctypes.c_void_p(FAKE + 2 * big), None) == 4
+    assert L.hamming_encode_secded(6, None, 8, None, None) == 2
+    assert L.hamming_channel_generate_secded(6, 1, 0, 8, 0, 0, 2 ** 32 + 1, ctypes.c_void_p(FAKE), None) == 5
