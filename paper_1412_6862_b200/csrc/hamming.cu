@@ -342,19 +342,24 @@ struct DecodeOp {
       }
       const uint32_t s = syndrome_cw<M>(lo, hi);  // a2
       uint32_t flag = 0;
-      bool flip = true;
       if constexpr (EXT) {  // overall parity P decides: P = 1 correct, P = 0 and s != 0 detect
         uint32_t par;
         if constexpr (M == 6) par = __popc(lo ^ hi) & 1u;
         else if constexpr (M == 5) par = __popc(lo) & 1u;
         else par = __popc(lo & ((1u << CW_BITS) - 1u)) & 1u;
-        flip = par != 0;
-        flag = (par << 6) | ((par == 0 && s != 0) ? 0x80u : 0u);
-      }
-      if constexpr (M <= 5) {  // a3 (s = 0 flips bit 0: the dummy or the parity bit)
-        lo ^= flip ? (1u << s) : 0u;
+        if constexpr (M <= 5) {  // a3: flip position s only when P = 1 (s = 0: the parity bit)
+          lo ^= par << s;
+        } else {
+          const uint64_t f = static_cast<uint64_t>(par) << s;
+          lo ^= static_cast<uint32_t>(f);
+          hi ^= static_cast<uint32_t>(f >> 32);
+        }
+        const uint32_t ded = ((s + 63u) >> 6) & (par ^ 1u);  // s != 0 (s <= 63) and P = 0
+        flag = (par << 6) | (ded << 7);
+      } else if constexpr (M <= 5) {  // a3 (s = 0 flips the dummy bit 0)
+        lo ^= 1u << s;
       } else {
-        const uint64_t f = flip ? (1ull << s) : 0ull;
+        const uint64_t f = 1ull << s;
         lo ^= static_cast<uint32_t>(f);
         hi ^= static_cast<uint32_t>(f >> 32);
       }
