@@ -1419,7 +1419,7 @@ hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void* rx_
   a.status = status_dev;
   a.counts = counts_dev;
   a.n_packets = n_packets;
-  return launch_packets<kPktDecode>(g, a, st);
+  return launch_packets_decode(g, a, st);
 }
 
 hamming_status hamming_encode_packets(uint32_t msg_bytes, int t, const void* msg_dev, uint64_t msg_stride,

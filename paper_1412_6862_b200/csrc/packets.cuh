@@ -88,29 +88,6 @@ __device__ __forceinline__ uint32_t xor_of_indices(uint32_t x) {
 // -- is still inside the buffer and every chunk is one funnel shift.
 constexpr uint32_t kPadBits = 128;
 
-// Syndrome of segment (off, n): positions 1..n are stream bits off .. off+n-1.
-// Chunk j = positions 32j .. 32j+31 = buffer bits off + kPadBits - 1 + 32j:
-// a constant shift for every chunk.  Warp-collective; every lane returns s.
-__device__ __forceinline__ uint32_t segment_syndrome(const uint32_t* w, uint32_t off, uint32_t n, int lane) {
-  const uint32_t chunks = (n + 32) / 32;  // positions 0..n
-  const uint32_t o = off + kPadBits - 1;
-  const uint32_t qb = o >> 5, rb = o & 31u;
-  uint32_t X = 0, P = 0;
-  for (uint32_t j = lane; j < chunks; j += 32) {
-    uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb);
-    const uint32_t last = n - 32 * j;  // highest position index inside this chunk
-    x &= (last < 31 ? low_mask(last + 1) : 0xFFFFFFFFu) & (j == 0 ? 0xFFFFFFFEu : 0xFFFFFFFFu);
-    X ^= x;
-    P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
-  }
-#pragma unroll
-  for (int sh = 16; sh > 0; sh >>= 1) {
-    X ^= __shfl_xor_sync(0xffffffffu, X, sh);
-    P ^= __shfl_xor_sync(0xffffffffu, P, sh);
-  }
-  return P ^ xor_of_indices(X);
-}
-
 // Data index -> run: the data bits of run j (positions 2^j+1 .. 2^(j+1)-1) are
 // d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2.  Closed form
 // j = floor(log2(d + floor(log2(d + 2)) + 2)) (checked exhaustively for
@@ -118,31 +95,6 @@ __device__ __forceinline__ uint32_t segment_syndrome(const uint32_t* w, uint32_t
 __device__ __forceinline__ uint32_t run_of(uint32_t d) {
   const uint32_t j0 = 31u - __clz(d + 2);
   return 31u - __clz(d + j0 + 2);
-}
-
-// Message word mw (bits 32 mw .. 32 mw + 31 of the packet message) restricted
-// to segment (off, k, moff): the data bits of that segment, RR'd, in place.
-__device__ __forceinline__ uint32_t segment_msg_word(const uint32_t* w, uint32_t off, uint32_t k, uint32_t moff,
-                                                     uint32_t mw) {
-  const uint32_t b0 = max(32u * mw, moff), b1 = min(32u * mw + 32u, moff + k);
-  uint32_t d = b0 - moff;
-  uint32_t j = run_of(d);
-  uint32_t run_end = (2u << j) - j - 2;  // first data index of the next run
-  if (b1 - moff <= run_end) {            // one run: one funnel-shifted slice
-    const uint32_t x = sm_bits32(w, off + kPadBits + d + j + 1);
-    return (b1 - b0 == 32u) ? x : ((x & low_mask(b1 - b0)) << (b0 - 32u * mw));
-  }
-  uint32_t out = 0;
-  uint32_t b = b0;
-  while (b < b1) {
-    const uint32_t take = min(b1, moff + run_end) - b;
-    out |= (sm_bits32(w, off + kPadBits + d + j + 1) & low_mask(take)) << (b - 32u * mw);
-    b += take;
-    d += take;
-    ++j;
-    run_end = (2u << j) - j - 2;
-  }
-  return out;
 }
 
 // Encoder side: codeword word cw (positions 32 cw .. 32 cw + 31) of segment
@@ -164,50 +116,6 @@ __device__ __forceinline__ uint32_t segment_code_word(const uint32_t* msg, uint3
     p = run_end;
   }
   return out;
-}
-
-// Decode the packet held in shared memory `w` (from bit kPadBits on) into the
-// shared message buffer `mbuf`; returns the packet status and writes the
-// syndromes.  Words strictly inside a segment's last run -- most of them --
-// are one funnel shift with a per-segment constant offset; the rest take the
-// general run walk.  Only a segment's first message word can already hold
-// the previous segment's bits, so it alone is OR-ed.  Warp-collective.
-__device__ __forceinline__ uint32_t decode_packet_warp(const PacketGeom& g, uint32_t* w, uint32_t* mbuf, int lane,
-                                                       uint16_t* syn_out, uint32_t& n_corr, uint32_t& n_fail) {
-  uint32_t status = 0;
-  for (uint32_t i = 0; i < g.t; ++i) {
-    const uint32_t off = g.off[i], n = g.n[i], k = g.k[i], moff = g.moff[i], r = g.r[i];
-    const uint32_t s = segment_syndrome(w, off, n, lane);
-    if (s != 0 && s <= n) {  // EC: flip position s
-      if (lane == 0) {
-        const uint32_t b = off + kPadBits + s - 1;
-        w[b >> 5] ^= 1u << (b & 31);
-      }
-      status = max(status, 1u);
-      ++n_corr;
-    } else if (s > n) {
-      status = 2;
-      ++n_fail;
-    }
-    __syncwarp();
-    if (syn_out != nullptr && lane == 0) syn_out[i] = static_cast<uint16_t>(s);
-    // RR + merger
-    const uint32_t J = r - 1;                                    // last run
-    const uint32_t last_lo = moff + (1u << J) - J - 1;           // first message bit of the last run
-    const uint32_t fast_lo = (last_lo + 31) / 32, fast_hi = (moff + k) / 32;  // whole words inside it
-    const uint32_t C = off + kPadBits + J + 1 - moff;            // buffer bit = message bit + C
-    const uint32_t cq = C >> 5, cr = C & 31u;
-    const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
-    for (uint32_t mw = mw0 + lane; mw < mw1; mw += 32) {
-      uint32_t v;
-      if (mw >= fast_lo && mw < fast_hi && r >= 2) v = __funnelshift_r(w[mw + cq], w[mw + cq + 1], cr);
-      else v = segment_msg_word(w, off, k, moff, mw);
-      if (mw == mw0 && (moff & 31u)) mbuf[mw] |= v;
-      else mbuf[mw] = v;
-    }
-    __syncwarp();
-  }
-  return status;
 }
 
 // Encode the message in shared memory `msg` into the packet stream `w`
@@ -259,7 +167,7 @@ __device__ __forceinline__ uint64_t pkt_mix(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-enum PacketMode { kPktDecode = 0, kPktEncode = 1, kPktGenerate = 2 };
+enum PacketMode { kPktEncode = 1, kPktGenerate = 2 };
 
 struct PacketArgs {
   const uint8_t* in;   // decode: received packets; encode: messages
@@ -276,114 +184,53 @@ struct PacketArgs {
   uint8_t* gen_msg;    // generate: sent messages (nullable), msg_bytes apart
 };
 
+// Encoder / synthetic channel: one warp per packet (not on the hot path).
 template <int MODE>
 __global__ void __launch_bounds__(kPktWarps * 32)
     packets_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ PacketArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ unsigned long long cta_counts[2];
-  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t kBufs = (MODE == kPktDecode) ? 2 : 1;
-  uint8_t* wb = smem + warp * (kBufs * g.in_cap + g.msg_cap);
-  uint32_t* w = reinterpret_cast<uint32_t*>(wb);                          // packet stream (encode/generate)
-  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kBufs * g.in_cap);    // message
-  uint64_t* bars = bars_all + warp * 2;
-  if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
-  __syncthreads();
+  uint8_t* wb = smem + warp * (g.in_cap + g.msg_cap);
+  uint32_t* w = reinterpret_cast<uint32_t*>(wb);                  // packet stream
+  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + g.in_cap);    // message
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
-  const uint64_t pol = policy_evict_first();
-  uint32_t n_corr = 0, n_fail = 0;
-  if constexpr (MODE == kPktDecode) {
-    if (lane == 0) {
-      mbar_init(&bars[0], 1);
-      mbar_init(&bars[1], 1);
-      fence_mbar_init();
-      for (uint32_t b = 0; b < 2; ++b) {
-        const uint64_t pk = gw + b * nw;
-        if (pk < a.n_packets) {
-          mbar_arrive_expect_tx(&bars[b], g.in_bytes);
-          bulk_g2s(wb + b * g.in_cap + 16, a.in + pk * a.in_stride, g.in_bytes, &bars[b], pol);
-        }
-      }
-    }
-    __syncwarp();
-  }
-  uint32_t it = 0;
-  for (uint64_t pk = gw; pk < a.n_packets; pk += nw, ++it) {
-    if constexpr (MODE == kPktDecode) {
-      const uint32_t buf = it & 1u;
-      uint32_t* wcur = reinterpret_cast<uint32_t*>(wb + buf * g.in_cap);
-      mbar_wait(&bars[buf], (it >> 1) & 1u);
-      const uint32_t st = decode_packet_warp(g, wcur, mbuf, lane, a.syn ? a.syn + pk * g.t : nullptr, n_corr, n_fail);
-      if (lane == 0) {  // the buffer is consumed: prefetch the packet two steps ahead into it
-        const uint64_t nx = pk + 2 * nw;
-        if (nx < a.n_packets) {
-          mbar_arrive_expect_tx(&bars[buf], g.in_bytes);
-          bulk_g2s(reinterpret_cast<uint8_t*>(wcur) + 16, a.in + nx * a.in_stride, g.in_bytes, &bars[buf], pol);
-        }
-      }
-      if (a.status != nullptr && lane == 0) a.status[pk] = static_cast<uint8_t>(st);
-      uint8_t* dst = a.out + pk * a.out_stride;
-      if (((reinterpret_cast<uintptr_t>(a.out) | a.out_stride | g.msg_bytes) & 15u) == 0) {
-        for (uint32_t i = lane; i < g.msg_bytes / 16; i += 32)
-          reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
-      } else {
-        const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
-        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[i];
-      }
-      __syncwarp();
+  for (uint64_t pk = gw; pk < a.n_packets; pk += nw) {
+    uint8_t* mb = reinterpret_cast<uint8_t*>(mbuf);
+    if constexpr (MODE == kPktEncode) {
+      const uint8_t* src = a.in + pk * a.in_stride;
+      for (uint32_t i = lane; i < g.msg_bytes; i += 32) mb[i] = src[i];
     } else {
-      uint8_t* mb = reinterpret_cast<uint8_t*>(mbuf);
-      if constexpr (MODE == kPktEncode) {
-        const uint8_t* src = a.in + pk * a.in_stride;
-        for (uint32_t i = lane; i < g.msg_bytes; i += 32) mb[i] = src[i];
-      } else {
-        const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
-        for (uint32_t q = lane; q < (g.msg_bytes + 7) / 8; q += 32) {
-          const uint64_t u = pkt_mix(key + (static_cast<uint64_t>(q) + 1) * 0x9E3779B97F4A7C15ull);
-          for (uint32_t b = 0; b < 8 && 8 * q + b < g.msg_bytes; ++b) mb[8 * q + b] = static_cast<uint8_t>(u >> (8 * b));
-        }
-      }
-      for (uint32_t i = g.msg_bytes + lane; i < g.msg_cap; i += 32) mb[i] = 0;
-      __syncwarp();
-      encode_packet_warp(g, mbuf, w, lane);
-      if constexpr (MODE == kPktGenerate) {
-        const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
-        const uint32_t W = (g.msg_bytes + 7) / 8;
-        if (lane < static_cast<int>(g.t)) {
-          const uint64_t ue = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 1) * 0x9E3779B97F4A7C15ull);
-          const uint64_t up = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 2) * 0x9E3779B97F4A7C15ull);
-          if (a.all || ue < a.thresh) {
-            const uint32_t p = 1u + __umulhi(static_cast<uint32_t>(up), g.n[lane]);
-            const uint32_t b = g.off[lane] + p - 1;
-            atomicXor(&w[b >> 5], 1u << (b & 31));
-          }
-        }
-        __syncwarp();
-        if (a.gen_msg != nullptr) {
-          uint8_t* gm = a.gen_msg + pk * g.msg_bytes;
-          for (uint32_t i = lane; i < g.msg_bytes; i += 32) gm[i] = mb[i];
-        }
-      }
-      uint4* dst = reinterpret_cast<uint4*>(a.out + pk * a.out_stride);
-      for (uint32_t i = lane; i < g.in_bytes / 16; i += 32) dst[i] = reinterpret_cast<const uint4*>(w)[i];
-      __syncwarp();
-    }
-  }
-  if constexpr (MODE == kPktDecode) {
-    if (a.counts != nullptr) {
-      // s is warp-uniform, so every lane holds the warp's counts: lane 0 adds them
-      if (lane == 0) {
-        if (n_corr) atomicAdd(&cta_counts[0], static_cast<unsigned long long>(n_corr));
-        if (n_fail) atomicAdd(&cta_counts[1], static_cast<unsigned long long>(n_fail));
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (cta_counts[0]) atomicAdd(&a.counts[0], cta_counts[0]);
-        if (cta_counts[1]) atomicAdd(&a.counts[1], cta_counts[1]);
+      const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
+      for (uint32_t q = lane; q < (g.msg_bytes + 7) / 8; q += 32) {
+        const uint64_t u = pkt_mix(key + (static_cast<uint64_t>(q) + 1) * 0x9E3779B97F4A7C15ull);
+        for (uint32_t b = 0; b < 8 && 8 * q + b < g.msg_bytes; ++b) mb[8 * q + b] = static_cast<uint8_t>(u >> (8 * b));
       }
     }
+    for (uint32_t i = g.msg_bytes + lane; i < g.msg_cap; i += 32) mb[i] = 0;
+    __syncwarp();
+    encode_packet_warp(g, mbuf, w, lane);
+    if constexpr (MODE == kPktGenerate) {
+      const uint64_t key = pkt_mix(a.seed + (a.g_first + pk + 1) * 0x9E3779B97F4A7C15ull);
+      const uint32_t W = (g.msg_bytes + 7) / 8;
+      if (lane < static_cast<int>(g.t)) {
+        const uint64_t ue = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 1) * 0x9E3779B97F4A7C15ull);
+        const uint64_t up = pkt_mix(key + (static_cast<uint64_t>(W) + 2 * lane + 2) * 0x9E3779B97F4A7C15ull);
+        if (a.all || ue < a.thresh) {
+          const uint32_t p = 1u + __umulhi(static_cast<uint32_t>(up), g.n[lane]);
+          const uint32_t b = g.off[lane] + p - 1;
+          atomicXor(&w[b >> 5], 1u << (b & 31));
+        }
+      }
+      __syncwarp();
+      if (a.gen_msg != nullptr) {
+        uint8_t* gm = a.gen_msg + pk * g.msg_bytes;
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) gm[i] = mb[i];
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(a.out + pk * a.out_stride);
+    for (uint32_t i = lane; i < g.in_bytes / 16; i += 32) dst[i] = reinterpret_cast<const uint4*>(w)[i];
+    __syncwarp();
   }
 }
 
@@ -392,7 +239,7 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const size_t smem = static_cast<size_t>(kPktWarps) * ((MODE == kPktDecode ? 2 : 1) * g.in_cap + g.msg_cap);
+  const size_t smem = static_cast<size_t>(kPktWarps) * (g.in_cap + g.msg_cap);
   auto kfn = packets_kernel<MODE>;
   e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets)");
@@ -405,6 +252,267 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
     kfn<<<grid, kPktWarps * 32, smem, st>>>(g, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "packets kernel launch");
+  }
+  g_launches = grid > 0 ? 1 : 0;
+  g_grid = grid;
+  return HAMMING_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Decode engine for long (shortened) codewords: a warp stages a BATCH of
+// consecutive packets (TMA bulk, double-buffered) and decodes its items -- the
+// (packet, segment) codewords -- with GROUPS of L lanes per item (L a power
+// of two chosen from the codeword length: short segments take one or two
+// lanes each, an 8013-bit segment takes the whole warp).  Within a group the
+// chunks of the syndrome and the words of the message are dealt round-robin;
+// the group XOR-reduces with L-1 shuffles.  Message words wholly inside an
+// item are stored, words shared with a neighbouring item are OR-ed atomically
+// into the batch's shared message buffer, which the warp then writes out.
+// ---------------------------------------------------------------------------
+struct BatchGeom {
+  uint32_t G;          // packets per batch
+  uint32_t L;          // lanes per item (power of two)
+  uint32_t in_cap;     // bytes per input buffer: 16 pad + G*stride + 16 slack
+  uint32_t msg_cap;    // bytes of the message buffer (16-aligned, + slack)
+  uint32_t warp_bytes; // 2*in_cap + msg_cap + 16*G (status words)
+};
+
+hamming_status batch_geom(const PacketGeom& g, uint64_t stride, BatchGeom& b) {
+  uint32_t maxn = 0;
+  for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
+  const uint32_t chunks = (maxn + 32) / 32;
+  uint32_t L = 1;
+  while (L < 32 && L * 8 < chunks) L *= 2;
+#ifndef HAM_PKT_BUDGET
+#define HAM_PKT_BUDGET (10 * 1024)
+#endif
+  const uint64_t budget = HAM_PKT_BUDGET;  // shared bytes per warp (tuned: tools/tune_shapes.py packets)
+  const uint64_t per = 2 * stride + (g.msg_bytes + 3) / 4 * 4 + 4;
+  uint64_t G = budget > 96 ? (budget - 96) / per : 1;
+  G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
+  b.G = static_cast<uint32_t>(G);
+  b.L = L;
+  b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
+  b.msg_cap = static_cast<uint32_t>((G * g.msg_bytes + 15) / 16 * 16 + 16);
+  b.warp_bytes = 2 * b.in_cap + b.msg_cap + static_cast<uint32_t>(16 * ((G * 4 + 15) / 16));
+  if (b.warp_bytes * 2ull > 227ull * 1024) return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
+  return HAMMING_OK;
+}
+
+// Syndrome of item (off, n) by a group of L lanes (rank q); all 32 lanes call
+// it together (inactive groups pass active = false).  Interior chunks need no
+// mask; the group's rank-0 lane adds the first chunk (position 0 masked off)
+// and the last one (positions past n masked off).
+__device__ __forceinline__ uint32_t group_syndrome(const uint32_t* w, uint32_t off, uint32_t n, bool active,
+                                                   uint32_t q, uint32_t L) {
+  const uint32_t chunks = active ? (n + 32) / 32 : 0;
+  const uint32_t o = off + kPadBits - 1;
+  const uint32_t qb = o >> 5, rb = o & 31u;
+  uint32_t X = 0, P = 0;
+  for (uint32_t j = 1 + q; j + 1 < chunks; j += L) {
+    const uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb);
+    X ^= x;
+    P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
+  }
+  if (active && q == 0) {
+    uint32_t x0 = __funnelshift_r(w[qb], w[qb + 1], rb) & 0xFFFFFFFEu;
+    if (chunks == 1) x0 &= low_mask(n + 1);
+    X ^= x0;
+    if (chunks > 1) {
+      const uint32_t j = chunks - 1;
+      const uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb) & low_mask(n - 32 * j + 1);
+      X ^= x;
+      P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
+    }
+  }
+  for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
+    X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+    P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+  }
+  return P ^ xor_of_indices(X);
+}
+
+// Redundancy removal + merger for one item by its group: lane q builds message
+// words mw0 + q, mw0 + q + L, ...  Data index d sits in run j at buffer bit
+// off + kPadBits + d + j + 1; each lane tracks the run of its current word
+// incrementally (runs only get longer), so a word inside one run costs one
+// funnel shift; words straddling a run boundary (at most r - 1 of them) take
+// the piecewise path.  Words wholly inside the item are stored, the item's
+// first and last word (shared with neighbours) are OR-ed atomically.  fb =
+// message bit to flip (the corrected data bit) or ~0.
+__device__ __forceinline__ void group_rr(const uint32_t* w, uint32_t* mbuf, uint32_t off, uint32_t k,
+                                         uint32_t moff, uint32_t fb, uint32_t q, uint32_t L) {
+  const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
+  const uint32_t base = off + kPadBits + 1;  // buffer bit of data index d in run j: base + d + j
+  uint32_t j = 1, run_end = 1;               // run j covers data indices [.., run_end)
+  for (uint32_t mw = mw0 + q; mw < mw1; mw += L) {
+    const uint32_t b0 = max(32u * mw, moff), b1 = min(32u * mw + 32u, moff + k);
+    uint32_t d = b0 - moff;
+    while (d >= run_end) {  // advance to the run holding d
+      ++j;
+      run_end = (2u << j) - j - 2;
+    }
+    uint32_t v;
+    if (b1 - moff <= run_end) {  // one run: one funnel-shifted slice
+      v = sm_bits32(w, base + d + j);
+      if (b1 - b0 != 32u) v = (v & low_mask(b1 - b0)) << (b0 - 32u * mw);
+    } else {
+      v = 0;
+      uint32_t b = b0, jj = j, re = run_end;
+      while (b < b1) {
+        const uint32_t take = min(b1, moff + re) - b;
+        v |= (sm_bits32(w, base + d + jj) & low_mask(take)) << (b - 32u * mw);
+        b += take;
+        d += take;
+        ++jj;
+        re = (2u << jj) - jj - 2;
+      }
+    }
+    if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
+    if (32 * mw >= moff && 32 * mw + 32 <= moff + k) mbuf[mw] = v;
+    else atomicOr(&mbuf[mw], v);
+  }
+}
+
+__global__ void __launch_bounds__(kPktWarps * 32)
+    packets_decode_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ BatchGeom bg,
+                          const __grid_constant__ PacketArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ unsigned long long cta_counts[2];
+  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wb = smem + warp * bg.warp_bytes;
+  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap);
+  uint32_t* pst = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + bg.msg_cap);  // per-packet status
+  uint64_t* bars = bars_all + warp * 2;
+  if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t n_batches = (a.n_packets + bg.G - 1) / bg.G;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t L = bg.L, q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
+  const uint32_t groups = 32 / L;
+  const uint32_t msg_bits = g.msg_bytes * 8;
+  uint32_t n_corr = 0, n_fail = 0;
+  auto batch_bytes = [&](uint64_t b) -> uint32_t {
+    const uint64_t p0 = b * bg.G;
+    const uint64_t left = a.n_packets - p0;
+    return static_cast<uint32_t>((left < bg.G ? left : bg.G) * a.in_stride);
+  };
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    for (uint32_t s = 0; s < 2; ++s) {
+      const uint64_t b = gw + s * nw;
+      if (b < n_batches) {
+        mbar_arrive_expect_tx(&bars[s], batch_bytes(b));
+        bulk_g2s(wb + s * bg.in_cap + 16, a.in + b * bg.G * a.in_stride, batch_bytes(b), &bars[s], pol);
+      }
+    }
+  }
+  __syncwarp();
+  uint32_t it = 0;
+  for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
+    const uint32_t buf = it & 1u;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(wb + buf * bg.in_cap);
+    const uint64_t p0 = b * bg.G;
+    const uint64_t left = a.n_packets - p0;
+    const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
+    const uint32_t items = np * g.t;
+    const uint32_t mwords = (np * g.msg_bytes + 3) / 4;
+    for (uint32_t i = lane; i < mwords; i += 32) mbuf[i] = 0;
+    for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
+    mbar_wait(&bars[buf], (it >> 1) & 1u);
+    __syncwarp();
+    for (uint32_t base = 0; base < items; base += groups) {
+      const uint32_t item = base + gid;
+      const bool active = item < items;
+      const uint32_t pk = active ? item / g.t : 0, seg = active ? item % g.t : 0;
+      const uint32_t off = static_cast<uint32_t>(pk * a.in_stride * 8) + g.off[seg];
+      const uint32_t n = g.n[seg], k = g.k[seg];
+      const uint32_t moff = pk * msg_bits + g.moff[seg];
+      const uint32_t s = group_syndrome(w, off, n, active, q, L);
+      if (!active) continue;
+      const bool corr = s != 0 && s <= n;
+      const bool fail = s > n;
+      // data index of the corrected position (none for a parity position or no correction)
+      uint32_t ds = 0xFFFFFFFFu;
+      if (corr && (s & (s - 1)) != 0) ds = s - (31u - __clz(s)) - 2;
+      if (q == 0) {
+        if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
+        if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
+        n_corr += corr;
+        n_fail += fail;
+      }
+      group_rr(w, mbuf, off, k, moff, ds == 0xFFFFFFFFu ? 0xFFFFFFFFu : moff + ds, q, L);
+    }
+    __syncwarp();
+    if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
+      const uint64_t nx = b + 2 * nw;
+      if (nx < n_batches) {
+        mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
+        bulk_g2s(wb + buf * bg.in_cap + 16, a.in + nx * bg.G * a.in_stride, batch_bytes(nx), &bars[buf], pol);
+      }
+    }
+    // write the batch's messages and statuses
+    const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
+    if (a.out_stride == g.msg_bytes && ((reinterpret_cast<uintptr_t>(a.out) | (p0 * g.msg_bytes)) & 15u) == 0) {
+      uint8_t* dst = a.out + p0 * g.msg_bytes;
+      const uint32_t nb = np * g.msg_bytes;
+      for (uint32_t i = lane; i < nb / 16; i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
+      for (uint32_t i = nb / 16 * 16 + lane; i < nb; i += 32) dst[i] = mb[i];
+    } else {
+      for (uint32_t pk = 0; pk < np; ++pk) {
+        uint8_t* dst = a.out + (p0 + pk) * a.out_stride;
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * g.msg_bytes + i];
+      }
+    }
+    if (a.status != nullptr)
+      for (uint32_t i = lane; i < np; i += 32) a.status[p0 + i] = static_cast<uint8_t>(pst[i]);
+    __syncwarp();
+  }
+  if (a.counts != nullptr) {
+    n_corr = __reduce_add_sync(0xffffffffu, n_corr);
+    n_fail = __reduce_add_sync(0xffffffffu, n_fail);
+    if (lane == 0) {
+      if (n_corr) atomicAdd(&cta_counts[0], static_cast<unsigned long long>(n_corr));
+      if (n_fail) atomicAdd(&cta_counts[1], static_cast<unsigned long long>(n_fail));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (cta_counts[0]) atomicAdd(&a.counts[0], cta_counts[0]);
+      if (cta_counts[1]) atomicAdd(&a.counts[1], cta_counts[1]);
+    }
+  }
+}
+
+hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, cudaStream_t st) {
+  BatchGeom bg;
+  hamming_status rc = batch_geom(g, a.in_stride, bg);
+  if (rc != HAMMING_OK) return rc;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const size_t smem = static_cast<size_t>(kPktWarps) * bg.warp_bytes;
+  if (smem > 227 * 1024) return set_err(HAMMING_E_ARG, "packets: shared memory budget exceeded");
+  e = cudaFuncSetAttribute(packets_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets decode)");
+  // ask for the full shared-memory carveout so several CTAs fit per SM
+  e = cudaFuncSetAttribute(packets_decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, packets_decode_kernel, kPktWarps * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets decode)");
+  const uint64_t batches = (a.n_packets + bg.G - 1) / bg.G;
+  const uint64_t want = (batches + kPktWarps - 1) / kPktWarps;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+  if (grid > 0) {
+    packets_decode_kernel<<<grid, kPktWarps * 32, smem, st>>>(g, bg, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "packets decode launch");
   }
   g_launches = grid > 0 ? 1 : 0;
   g_grid = grid;

@@ -18,6 +18,9 @@ VARIANTS = {
 }
 
 
+PKT_BUDGETS = [4096, 6144, 8192, 12288, 16384, 24576]
+
+
 def name(m, v):
     return f"m{m}_w{v[0]}_s{v[1]}_ip{v[2]}"
 
@@ -35,12 +38,21 @@ def build():
             # the other m keep their defaults
             defs = [f"HAM_W{m}={v[0]}", f"HAM_S{m}={v[1]}", f"HAM_IP{m}={'true' if v[2] else 'false'}"]
             jobs.append((os.path.join(OUT, name(m, v) + ".so"), defs))
+    if len(sys.argv) > 2 and sys.argv[2] == "packets":
+        jobs = [(os.path.join(OUT, f"pkt_{bud}.so"), [f"HAM_PKT_BUDGET={bud}"]) for bud in PKT_BUDGETS]
     with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
         for path in ex.map(lambda j: b.build(force=True, out=j[0], defines=j[1]), jobs):
             print("built", path, flush=True)
 
 
 def run():
+    if len(sys.argv) > 2 and sys.argv[2] == "packets":
+        for bud in PKT_BUDGETS:
+            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{bud}.so"))
+            print("budget", bud, flush=True)
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "1200",
+                            "2000", "--t", "2", "6"], env=env)
+        return
     for m, vs in VARIANTS.items():
         for v in vs:
             path = os.path.join(OUT, name(m, v) + ".so")
