@@ -8,7 +8,11 @@
  * and redundancy remover (RR)" (Fig. 1), the syndrome ("checksum
  * vector") being the modulo-2 sum over each index set I_j (P:L98, P:L160
  * Algorithm 1 Step 4).  This library decodes packets of concatenated perfect
- * (n, k) = (2^m - 1, 2^m - 1 - m) codewords, m in [2, 6].
+ * (n, k) = (2^m - 1, 2^m - 1 - m) codewords, m in [2, 8] (m = 7, 8 -- the
+ * (127,120) and (255,247) codes of SURVEY.md 8(f) f4 -- through the long-
+ * codeword engine; encode and the synthetic channel cover m in [2, 6]),
+ * extended-Hamming (SECDED) codewords, and the paper's own packets of
+ * shortened codes.
  *
  * Stream layout (readings R3, R4):
  *   - stream bit b is bit (b & 7) of byte b >> 3 (LSB-first), i.e. bit
@@ -45,7 +49,7 @@ extern "C" {
 
 typedef enum {
     HAMMING_OK = 0,
-    HAMMING_E_INVALID_M = 1,   /* m not in [2, 6] */
+    HAMMING_E_INVALID_M = 1,   /* m out of range for the entry point */
     HAMMING_E_NULL = 2,        /* a required pointer is NULL while n_codewords > 0 */
     HAMMING_E_MISALIGNED = 3,  /* a device buffer is not 16-byte aligned */
     HAMMING_E_OVERLAP = 4,     /* input and output ranges overlap (no in-place) */
@@ -63,7 +67,7 @@ typedef enum {
  *   the k bits at non-power-of-two positions are kept, in order (P:L59 RR)
  *   and written to data bits [c*k, c*k + k)                     (P:L68 merger)
  * Arguments:
- *   m            code order, n = 2^m - 1, k = n - m, 2 <= m <= 6.
+ *   m            code order, n = 2^m - 1, k = n - m, 2 <= m <= 8.
  *   rx_dev       hamming_coded_bytes(m, N) bytes, 16-byte aligned; pad bits
  *                past n*N in the last byte are ignored.  Never written.
  *   n_codewords  N (64-bit; 0 is a valid no-op that sets *corrected = 0).
@@ -76,8 +80,8 @@ typedef enum {
  *                multi-bit errors included (reading R10).
  *   stream       cudaStream_t or NULL.
  * Buffers must not overlap.  With a 2-bit error the decoder deterministically
- * miscorrects (reading R9); for m <= 6 no syndrome exceeds n, so there is no
- * uncorrectable status (reading R8). */
+ * miscorrects (reading R9); for perfect codes no syndrome exceeds n, so there
+ * is no uncorrectable status (reading R8). */
 hamming_status hamming_decode(int m, const void *rx_dev, uint64_t n_codewords,
                               void *data_dev, uint8_t *syndromes_dev,
                               unsigned long long *corrected_dev, void *stream);

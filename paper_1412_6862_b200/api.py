@@ -20,8 +20,10 @@ TILE = 1024  # codewords per warp tile of the decode kernel
 
 
 def code_nk(m: int) -> tuple[int, int]:
-    if not 2 <= m <= 6:
-        raise ValueError("m must be in [2, 6]")
+    """(n, k) of the perfect code of order m; decode takes m in [2, 8],
+    encode / the synthetic channel m in [2, 6]."""
+    if not 2 <= m <= 8:
+        raise ValueError("m must be in [2, 8]")
     n = (1 << m) - 1
     return n, n - m
 

@@ -1009,8 +1009,12 @@ hamming_status ensure_lut15(int dev) {
   return HAMMING_OK;
 }
 
+hamming_status launch_long_decode(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
+                                  unsigned long long* counter, cudaStream_t st, bool accumulate);
+
 hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
                                unsigned long long* counter, cudaStream_t st, bool accumulate) {
+  if (m == 7 || m == 8) return launch_long_decode(m, in, N, out, syn, counter, st, accumulate);
   const uint64_t n = (1ull << m) - 1, k = n - m;
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
   if (N < kSmallPacketCw) {
@@ -1080,13 +1084,13 @@ extern "C" {
 int hamming_abi_version(void) { return HAMMING_ABI_VERSION; }
 
 uint64_t hamming_coded_bytes(int m, uint64_t N) {
-  if (m < 2 || m > 6 || bits_overflow(m, N)) return 0;
+  if (m < 2 || m > 8 || bits_overflow(m, N)) return 0;
   const uint64_t n = (1ull << m) - 1;
   return (n * N + 7) / 8;
 }
 
 uint64_t hamming_data_bytes(int m, uint64_t N) {
-  if (m < 2 || m > 6 || bits_overflow(m, N)) return 0;
+  if (m < 2 || m > 8 || bits_overflow(m, N)) return 0;
   const uint64_t k = (1ull << m) - 1 - m;
   return (k * N + 7) / 8;
 }
@@ -1094,7 +1098,7 @@ uint64_t hamming_data_bytes(int m, uint64_t N) {
 const char* hamming_status_string(hamming_status s) {
   switch (s) {
     case HAMMING_OK: return "ok";
-    case HAMMING_E_INVALID_M: return "invalid m (must be 2..6)";
+    case HAMMING_E_INVALID_M: return "invalid m (decode: 2..8; encode/generate: 2..6; SECDED: 3..6)";
     case HAMMING_E_NULL: return "required pointer is NULL";
     case HAMMING_E_MISALIGNED: return "device buffer not 16-byte aligned";
     case HAMMING_E_OVERLAP: return "input and output buffers overlap";
@@ -1113,7 +1117,7 @@ hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_
                               unsigned long long* corrected_dev, void* stream) {
   g_launches = 0;
   g_grid = 0;
-  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_decode: m must be in [2, 6]");
+  if (m < 2 || m > 8) return set_err(HAMMING_E_INVALID_M, "hamming_decode: m must be in [2, 8]");
   if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_decode: n * n_codewords overflows");
   if (corrected_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_decode: corrected is NULL");
   if (N > 0 && (rx_dev == nullptr || data_dev == nullptr))
@@ -1188,7 +1192,7 @@ hamming_status hamming_channel_generate(int m, uint64_t seed, uint64_t c_first, 
 }
 
 size_t hamming_host_workspace_bytes(int m, uint64_t chunk_codewords, int n_streams, int with_syndromes) {
-  if (m < 2 || m > 6 || n_streams < 1 || n_streams > 4 || chunk_codewords == 0 ||
+  if (m < 2 || m > 8 || n_streams < 1 || n_streams > 4 || chunk_codewords == 0 ||
       bits_overflow(m, chunk_codewords))
     return 0;
   return static_cast<size_t>(256 + n_streams * host_slot_layout(m, chunk_codewords, with_syndromes).slot);
@@ -1199,7 +1203,7 @@ hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void*
                                    uint64_t chunk, int n_streams) {
   g_launches = 0;
   g_grid = 0;
-  if (m < 2 || m > 6) return set_err(HAMMING_E_INVALID_M, "hamming_decode_host: m must be in [2, 6]");
+  if (m < 2 || m > 8) return set_err(HAMMING_E_INVALID_M, "hamming_decode_host: m must be in [2, 8]");
   if (bits_overflow(m, N)) return set_err(HAMMING_E_RANGE, "hamming_decode_host: size overflows");
   if (corrected_host == nullptr || workspace_dev == nullptr)
     return set_err(HAMMING_E_NULL, "hamming_decode_host: corrected or workspace is NULL");

@@ -518,3 +518,152 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   g_grid = grid;
   return HAMMING_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Longer perfect codes, m = 7, 8 ((127,120), (255,247)):
+// the same item engine over a stream of codewords -- a batch is 128
+// codewords (16n input bytes, 16k output bytes, both 16-byte aligned), items
+// are codewords (off = c n, moff = c k), one lane per codeword.
+// ---------------------------------------------------------------------------
+struct LongArgs {
+  const uint8_t* in;
+  uint8_t* out;
+  uint8_t* syn;
+  unsigned long long* counter;
+  uint64_t N, in_total, out_total;
+  uint32_t n, k, store_count;
+};
+
+constexpr uint32_t kLongBatch = 128;
+
+__global__ void __launch_bounds__(kPktWarps * 32)
+    long_decode_kernel(const __grid_constant__ LongArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ unsigned long long cta_count;
+  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t in_b = 16 * a.n, out_b = 16 * a.k;
+  const uint32_t in_cap = 16 + in_b + 16, msg_cap = out_b + 16;
+  uint8_t* wb = smem + warp * (2 * in_cap + msg_cap);
+  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * in_cap);
+  uint64_t* bars = bars_all + warp * 2;
+  if (threadIdx.x == 0) cta_count = 0;
+  __syncthreads();
+  const uint64_t n_full = a.N / kLongBatch;
+  const uint64_t n_batches = (a.N + kLongBatch - 1) / kLongBatch;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  const uint64_t pol = policy_evict_first();
+  uint32_t cnt = 0;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    for (uint32_t s = 0; s < 2; ++s) {
+      const uint64_t b = gw + s * nw;
+      if (b < n_full) {
+        mbar_arrive_expect_tx(&bars[s], in_b);
+        bulk_g2s(wb + s * in_cap + 16, a.in + b * in_b, in_b, &bars[s], pol);
+      }
+    }
+  }
+  __syncwarp();
+  uint32_t it = 0;
+  for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
+    const uint32_t buf = it & 1u;
+    uint8_t* wbytes = wb + buf * in_cap;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(wbytes);
+    const bool full = b < n_full;
+    const uint32_t nb = full ? kLongBatch : static_cast<uint32_t>(a.N - b * kLongBatch);
+    for (uint32_t i = lane; i < (out_b + 3) / 4; i += 32) mbuf[i] = 0;
+    if (full) {
+      mbar_wait(&bars[buf], (it >> 1) & 1u);
+    } else {  // the ragged last batch: bounded loads (TMA needs whole 16-byte units)
+      const uint64_t ib0 = b * in_b, nbytes = a.in_total - ib0;
+      for (uint32_t i = lane; i < in_b; i += 32) wbytes[16 + i] = i < nbytes ? a.in[ib0 + i] : 0;
+    }
+    __syncwarp();
+    for (uint32_t c = lane; c < kLongBatch; c += 32) {  // all lanes take part in every round
+      const bool active = c < nb;
+      const uint32_t off = c * a.n, moff = c * a.k;
+      const uint32_t s = group_syndrome(w, off, a.n, active, 0, 1);
+      if (!active) continue;
+      uint32_t fb = 0xFFFFFFFFu;
+      if (s != 0 && (s & (s - 1)) != 0) fb = moff + s - (31u - __clz(s)) - 2;
+      group_rr(w, mbuf, off, a.k, moff, fb, 0, 1);
+      if (a.syn != nullptr) a.syn[b * kLongBatch + c] = static_cast<uint8_t>(s);
+      cnt += (s != 0);
+    }
+    __syncwarp();
+    if (lane == 0 && full) {  // buffer consumed: prefetch the batch two steps ahead
+      const uint64_t nx = b + 2 * nw;
+      if (nx < n_full) {
+        mbar_arrive_expect_tx(&bars[buf], in_b);
+        bulk_g2s(wbytes + 16, a.in + nx * in_b, in_b, &bars[buf], pol);
+      }
+    }
+    uint8_t* dst = a.out + b * out_b;
+    if (full) {
+      for (uint32_t i = lane; i < out_b / 16; i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
+    } else {
+      const uint64_t nbytes = a.out_total - b * out_b;
+      const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
+      for (uint32_t i = lane; i < nbytes; i += 32) dst[i] = mb[i];
+    }
+    __syncwarp();
+  }
+  if (a.counter != nullptr) {
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0 && cnt) atomicAdd(&cta_count, static_cast<unsigned long long>(cnt));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (a.store_count) *a.counter = cta_count;
+      else if (cta_count) atomicAdd(a.counter, cta_count);
+    }
+  }
+}
+
+hamming_status launch_long_decode(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
+                                  unsigned long long* counter, cudaStream_t st, bool accumulate) {
+  LongArgs a{};
+  a.n = (1u << m) - 1;
+  a.k = a.n - static_cast<uint32_t>(m);
+  a.in = in;
+  a.out = out;
+  a.syn = syn;
+  a.counter = counter;
+  a.N = N;
+  a.in_total = (static_cast<uint64_t>(a.n) * N + 7) / 8;
+  a.out_total = (static_cast<uint64_t>(a.k) * N + 7) / 8;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const size_t smem = static_cast<size_t>(kPktWarps) * (2 * (16 + 16 * a.n + 16) + 16 * a.k + 16);
+  e = cudaFuncSetAttribute(long_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(long decode)");
+  e = cudaFuncSetAttribute(long_decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, long_decode_kernel, kPktWarps * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy(long decode)");
+  const uint64_t batches = (N + kLongBatch - 1) / kLongBatch;
+  const uint64_t want = (batches + kPktWarps - 1) / kPktWarps;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+  a.store_count = (counter != nullptr && !accumulate && grid == 1) ? 1u : 0u;
+  if (counter != nullptr && !accumulate && !a.store_count) {
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+  }
+  if (grid > 0) {
+    long_decode_kernel<<<grid, kPktWarps * 32, smem, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "long decode launch");
+  } else if (counter != nullptr && !accumulate) {
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+  }
+  g_launches = grid > 0 ? 1 : 0;
+  g_grid = grid;
+  return HAMMING_OK;
+}

@@ -41,13 +41,13 @@ def test_library_is_sm100a_only(L):
 
 def test_abi_and_sizes(L):
     assert L.hamming_abi_version() == 1
-    for m in range(2, 7):
+    for m in range(2, 9):
         n = 2 ** m - 1
         k = n - m
         for N in (0, 1, 7, 8, 1023, 1024, 4681, 10 ** 12):
             assert ham.coded_bytes(m, N) == (n * N + 7) // 8
             assert ham.data_bytes(m, N) == (k * N + 7) // 8
-    assert ham.coded_bytes(7, 10) == 0 and ham.coded_bytes(1, 10) == 0
+    assert ham.coded_bytes(9, 10) == 0 and ham.coded_bytes(1, 10) == 0
     assert ham.coded_bytes(6, 2 ** 64 // 63 + 1) == 0      # overflow
     # the north-star shapes: a 4 KB (7,4) packet is 4681 codewords
     assert ham.coded_bytes(3, 4681) == 4096
@@ -68,7 +68,7 @@ def _call_decode(L, m, rx, N, data, syn, cnt):
 
 def test_decode_argument_validation(L):
     big = 1 << 30
-    assert _call_decode(L, 7, FAKE, 10, FAKE + big, FAKE + 2 * big, FAKE + 3 * big) == 1
+    assert _call_decode(L, 9, FAKE, 10, FAKE + big, FAKE + 2 * big, FAKE + 3 * big) == 1
     assert _call_decode(L, 1, FAKE, 10, FAKE + big, FAKE + 2 * big, FAKE + 3 * big) == 1
     assert _call_decode(L, 6, 0, 10, FAKE + big, 0, FAKE + 3 * big) == 2
     assert _call_decode(L, 6, FAKE, 10, 0, 0, FAKE + 3 * big) == 2
@@ -85,6 +85,7 @@ def test_decode_argument_validation(L):
 
 def test_other_entry_point_validation(L):
     assert L.hamming_encode(9, None, 5, None, None) == 1
+    assert L.hamming_encode(7, None, 5, None, None) == 1      # encode stops at m = 6
     assert L.hamming_encode(3, None, 5, None, None) == 2
     assert L.hamming_encode(3, ctypes.c_void_p(FAKE + 1), 5, ctypes.c_void_p(FAKE + (1 << 20)), None) == 3
     assert L.hamming_channel_generate(3, 1, 0, 5, 0, 0, 2 ** 32 + 1, ctypes.c_void_p(FAKE), None) == 5

@@ -169,3 +169,33 @@ def test_decode_host_pipeline_matches_oracle(oracle, m):
         syn_h = torch.zeros(N, dtype=torch.uint8).pin_memory()
         cnt = ham.decode_host(m, rx_h, N, data_h, syn_h, ws, chunk_codewords=chunk, n_streams=streams)
         assert_same(m, N, (data_h.numpy(), syn_h.numpy(), cnt), want)
+
+
+def _noisy_codewords(oracle, m, N, seed, p_flip=0.4):
+    """Oracle-encoded random data with random single/double flips applied by
+    numpy (channel simulation only)."""
+    n, k = oracle.code_nk(m)
+    rng = np.random.default_rng(seed)
+    data = rng.integers(0, 256, (k * N + 7) // 8, dtype=np.uint8)
+    rx = oracle.encode(m, data, N)
+    bits = np.unpackbits(rx, bitorder="little")
+    for c in np.nonzero(rng.random(N) < p_flip)[0]:
+        for p in rng.choice(n, size=int(rng.integers(1, 3)), replace=False):
+            bits[c * n + p] ^= 1
+    return np.packbits(bits, bitorder="little")[: rx.size]
+
+
+@pytest.mark.parametrize("m", [7, 8])
+@pytest.mark.parametrize("N", [1, 31, 127, 128, 129, 1000, 4097])
+def test_long_perfect_codes_match_oracle(oracle, m, N):
+    """(127,120) and (255,247) through the long-codeword engine."""
+    rx = _noisy_codewords(oracle, m, N, 1000 * m + N)
+    assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+@pytest.mark.parametrize("m", [7, 8])
+def test_long_perfect_codes_random_streams(oracle, m):
+    rng = np.random.default_rng(m)
+    for N in (5, 128 * 37 + 11):
+        rx = rng.integers(0, 256, ham.coded_bytes(m, N), dtype=np.uint8)
+        assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
