@@ -442,14 +442,81 @@ struct DecodeLut3Op {
 // in global memory, copied into shared memory at CTA start.
 __device__ __align__(16) uint16_t g_lut15[32768];
 
+// (31,26) half-word table: for a 15-bit chunk x (bit p-1 = position p) the
+// UNcorrected redundancy removal (bits 0..10), the syndrome contribution
+// XOR{p} (bits 11..14) and the parity of x (bit 15).
+__device__ __align__(16) uint16_t g_lut15raw[32768];
+
 __global__ void init_lut15_kernel() {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x < 32768) {
     uint32_t dlo, dhi;
-    const uint32_t s = decode_cw<4>(static_cast<uint32_t>(x) << 1, 0u, dlo, dhi);
+    const uint32_t v = static_cast<uint32_t>(x) << 1;
+    const uint32_t s = decode_cw<4>(v, 0u, dlo, dhi);
     g_lut15[x] = static_cast<uint16_t>(dlo | (s << 12));
+    uint32_t raw = 0;
+#pragma unroll
+    for (int g = 1; g < 4; ++g) raw |= (v >> (g + 2)) & dmask(g);
+    g_lut15raw[x] = static_cast<uint16_t>(raw | (s << 11) | ((static_cast<uint32_t>(__popc(x)) & 1u) << 15));
   }
 }
+
+// (31,26): a codeword is two 15-bit table lookups -- positions 1..15 and
+// positions 17..31 -- plus position 16:  s = S(lo) ^ S(hi) ^ 16 (parity(hi) ^
+// bit16), data = RR(lo) | hi << 11, corrected by a per-lane flip-mask table
+// F[s] (4 KB, conflict-free).  No POPC: the XU pipe, which bounds the
+// POPC decoder at m = 5, is left idle.
+struct DecodeLut5Op {
+  static constexpr int NCOUNT = 1;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
+  static constexpr int IN_W = 31, OUT_W = 26, IN_BITS = 31;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr int SHARED = 32768 * 2 + 32 * 32 * 4;
+  struct Args {};
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    const uint4* src = reinterpret_cast<const uint4*>(g_lut15raw);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    for (int i = tid; i < 32768 * 2 / 16; i += nth) dst[i] = src[i];
+    uint32_t* F = reinterpret_cast<uint32_t*>(sh + 32768 * 2);
+    for (int e = tid; e < 32 * 32; e += nth) {  // F[s][lane] = the data bit of position s (0 if parity)
+      const uint32_t v = (e >> 5) ? (1u << (e >> 5)) : 0u;  // a word with only position s set
+      uint32_t raw = 0;
+#pragma unroll
+      for (int g = 1; g < 5; ++g) raw |= (v >> (g + 2)) & dmask(g);
+      F[e] = raw;
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[31];
+#pragma unroll
+    for (int i = 0; i < 31; ++i) w[i] = in[i];
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[26];
+#pragma unroll
+    for (int i = 0; i < 26; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t alo = field_at(w, 31 * c, 1) & 0xFFFEu;       // positions 1..15, x 2
+      const uint32_t h = take_bits(w, 31 * c + 15);                 // bit 0 = position 16, 1.. = 17..31
+      const uint32_t elo = *reinterpret_cast<const uint16_t*>(sh + alo);
+      const uint32_t ehi = *reinterpret_cast<const uint16_t*>(sh + (h & 0xFFFEu));
+      const uint32_t t = elo ^ ehi;
+      const uint32_t s = ((t >> 11) & 0xFu) | ((((ehi >> 15) ^ h) & 1u) << 4);
+      const uint32_t f = *reinterpret_cast<const uint32_t*>(sh + 65536 + (s << 7) + lane4);
+      const uint32_t d = ((elo & 0x7FFu) | ((h << 10) & 0x3FFF800u)) ^ f;
+      put_bits(o, 26 * c, d, 26);
+      side[c >> 2] |= s << (8 * (c & 3));
+    }
+#pragma unroll
+    for (int i = 0; i < 26; ++i) out[i] = o[i];
+  }
+};
 
 struct DecodeLut4Op {
   static constexpr int NCOUNT = 1;
@@ -973,7 +1040,7 @@ bool bits_overflow(int m, uint64_t N) {
 #define HAM_S5 3
 #endif
 #ifndef HAM_IP5
-#define HAM_IP5 false
+#define HAM_IP5 true
 #endif
 #ifndef HAM_W6
 #define HAM_W6 8
@@ -1048,9 +1115,15 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       return Launcher<DecodeLut4Op, HAM_W4, HAM_S4, HAM_IP4>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                   accumulate);
     }
-    case 5:
-      return Launcher<DecodeOp<5>, HAM_W5, HAM_S5, HAM_IP5>::run(in, out, syn, N, ib, ob, counter, {}, st,
-                                                                 accumulate);
+    case 5: {
+      int dev = 0;
+      const cudaError_t e = cudaGetDevice(&dev);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+      const hamming_status rc = ensure_lut15(dev);
+      if (rc != HAMMING_OK) return rc;
+      return Launcher<DecodeLut5Op, HAM_W5, HAM_S5, HAM_IP5>::run(in, out, syn, N, ib, ob, counter, {}, st,
+                                                                  accumulate);
+    }
     case 6:
       return Launcher<DecodeOp<6>, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                  accumulate);

@@ -11,10 +11,10 @@ OUT = os.path.join(ROOT, "build", "tune")
 
 VARIANTS = {
     # m: list of (W, S, in_place)
-    3: [(16, 8, 1), (16, 6, 0), (32, 4, 1), (16, 12, 1)],
-    4: [(16, 4, 1), (12, 4, 0), (16, 5, 1), (8, 8, 1)],
-    5: [(16, 3, 1), (12, 3, 0), (12, 4, 1), (8, 6, 1), (8, 4, 0), (16, 2, 1)],
-    6: [(8, 3, 1), (7, 2, 0), (4, 6, 1), (8, 2, 1), (4, 5, 1)],
+    3: [(16, 12, 1), (32, 6, 1), (24, 8, 1), (8, 24, 1)],
+    4: [(8, 8, 1), (12, 6, 1), (4, 16, 1)],
+    5: [(8, 4, 1), (12, 3, 1), (16, 2, 1), (4, 8, 1), (8, 3, 1)],
+    6: [(8, 3, 1)],
 }
 
 
