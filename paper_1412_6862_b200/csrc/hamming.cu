@@ -177,6 +177,19 @@ __device__ __forceinline__ uint32_t count_nonzero_bytes(const uint32_t (&w)[8]) 
   return (acc * 0x01010101u) >> 24;  // four byte lanes of at most 8 each
 }
 
+// The same count with one POPC per word: for the table decoders, whose XU
+// pipe is otherwise idle and whose ALU pipe is the tighter one.
+__device__ __forceinline__ uint32_t count_nonzero_bytes_xu(const uint32_t (&w)[8]) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t t;
+    asm("mad.lo.u32 %0, %1, 1, 2139062143;" : "=r"(t) : "r"(w[i]));  // + 0x7F7F7F7F on the FMA pipe
+    c += __popc(t & 0x80808080u);
+  }
+  return c;
+}
+
 // --------------------------------------------------------- per-codeword math
 // Decode one codeword given as v = (lo, hi): bit p of v holds position p
 // (hi bit i = position 32 + i; hi unused for m <= 5).  Returns the syndrome s
@@ -400,7 +413,7 @@ __device__ __forceinline__ uint32_t insert_byte1(uint32_t word, uint32_t e, int 
 // syndrome << 8; lane l reads word [x][l], always its own bank (16 KB).
 struct DecodeLut3Op {
   static constexpr int NCOUNT = 1;
-  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
   static constexpr bool HAS_SIDE = true;
@@ -468,7 +481,7 @@ __global__ void init_lut15_kernel() {
 // POPC decoder at m = 5, is left idle.
 struct DecodeLut5Op {
   static constexpr int NCOUNT = 1;
-  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 31, OUT_W = 26, IN_BITS = 31;
   static constexpr bool HAS_SIDE = true;
@@ -520,7 +533,7 @@ struct DecodeLut5Op {
 
 struct DecodeLut4Op {
   static constexpr int NCOUNT = 1;
-  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes(sw); }
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 15, OUT_W = 11, IN_BITS = 15;
   static constexpr bool HAS_SIDE = true;
