@@ -332,41 +332,52 @@ __device__ __forceinline__ uint32_t group_syndrome(const uint32_t* w, uint32_t o
   return P ^ xor_of_indices(X);
 }
 
+// The first 57 data bits of an item (positions 3..63 -- runs 1..5, where
+// the run boundaries are dense) by the fixed compaction of the (63,57) code:
+// v = positions 0..63, groups g = 1..4 from the low word, positions 33..63
+// from the high word.  Bits past k are garbage and are masked by the caller.
+__device__ __forceinline__ uint64_t rr_head57(const uint32_t* w, uint32_t off) {
+  const uint32_t o = off + kPadBits - 1;  // buffer bit of position 0
+  const uint32_t q = o >> 5, r = o & 31u;
+  const uint32_t lo = __funnelshift_r(w[q], w[q + 1], r);
+  const uint32_t hi = __funnelshift_r(w[q + 1], w[q + 2], r);
+  uint32_t d = 0;
+#pragma unroll
+  for (int g = 1; g < 5; ++g) d |= (lo >> (g + 2)) & dmask(g);
+  return static_cast<uint64_t>(d) | (static_cast<uint64_t>(hi >> 1) << 26);
+}
+
 // Redundancy removal + merger for one item by its group: lane q builds message
 // words mw0 + q, mw0 + q + L, ...  Data index d sits in run j at buffer bit
-// off + kPadBits + d + j + 1; each lane tracks the run of its current word
-// incrementally (runs only get longer), so a word inside one run costs one
-// funnel shift; words straddling a run boundary (at most r - 1 of them) take
-// the piecewise path.  Words wholly inside the item are stored, the item's
-// first and last word (shared with neighbours) are OR-ed atomically.  fb =
-// message bit to flip (the corrected data bit) or ~0.
+// off + kPadBits + d + j + 1.  d < 57 comes from rr_head57; from d = 57 on
+// every run is >= 63 bits long, so a 32-bit window holds at most one run
+// boundary: the word is two funnel-shifted slices one bit apart, merged at the
+// boundary -- branch free.  Words wholly inside the item are stored, the
+// item's edge words (shared with neighbours) OR-ed atomically.  fb = message
+// bit to flip (the corrected data bit) or ~0.
 __device__ __forceinline__ void group_rr(const uint32_t* w, uint32_t* mbuf, uint32_t off, uint32_t k,
                                          uint32_t moff, uint32_t fb, uint32_t q, uint32_t L) {
   const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
-  const uint32_t base = off + kPadBits + 1;  // buffer bit of data index d in run j: base + d + j
-  uint32_t j = 1, run_end = 1;               // run j covers data indices [.., run_end)
+  uint64_t head = 0;
+  const bool need_head = q < 3;  // the words holding d < 57 are the first (at most) three
+  if (need_head) head = rr_head57(w, off);
   for (uint32_t mw = mw0 + q; mw < mw1; mw += L) {
-    const uint32_t b0 = max(32u * mw, moff), b1 = min(32u * mw + 32u, moff + k);
-    uint32_t d = b0 - moff;
-    while (d >= run_end) {  // advance to the run holding d
-      ++j;
-      run_end = (2u << j) - j - 2;
+    const uint32_t d0 = max(32u * mw, moff) - moff;
+    const uint32_t d1 = min(32u * mw + 32u, moff + k) - moff;
+    const uint32_t sh = moff + d0 - 32u * mw;  // bit of the word that receives d0
+    uint32_t v = 0;
+    if (d0 < 57u) {
+      const uint32_t e = min(d1, 57u);
+      v = (static_cast<uint32_t>(head >> d0) & low_mask(e - d0)) << sh;
     }
-    uint32_t v;
-    if (b1 - moff <= run_end) {  // one run: one funnel-shifted slice
-      v = sm_bits32(w, base + d + j);
-      if (b1 - b0 != 32u) v = (v & low_mask(b1 - b0)) << (b0 - 32u * mw);
-    } else {
-      v = 0;
-      uint32_t b = b0, jj = j, re = run_end;
-      while (b < b1) {
-        const uint32_t take = min(b1, moff + re) - b;
-        v |= (sm_bits32(w, base + d + jj) & low_mask(take)) << (b - 32u * mw);
-        b += take;
-        d += take;
-        ++jj;
-        re = (2u << jj) - jj - 2;
-      }
+    if (d1 > 57u) {
+      const uint32_t dd = max(d0, 57u);
+      const uint32_t j = run_of(dd);
+      const uint32_t nb = min(32u, (2u << j) - j - 2 - dd);  // bits before the next run starts
+      const uint32_t src = off + kPadBits + dd + j + 1;
+      const uint32_t x0 = sm_bits32(w, src), x1 = sm_bits32(w, src + 1);
+      const uint32_t part = ((x0 & low_mask(nb)) | (x1 & ~low_mask(nb))) & low_mask(d1 - dd);
+      v |= part << (sh + dd - d0);
     }
     if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
     if (32 * mw >= moff && 32 * mw + 32 <= moff + k) mbuf[mw] = v;
