@@ -347,41 +347,77 @@ __device__ __forceinline__ uint64_t rr_head57(const uint32_t* w, uint32_t off) {
   return static_cast<uint64_t>(d) | (static_cast<uint64_t>(hi >> 1) << 26);
 }
 
+// One message word of an item, general form (edge words, words holding
+// d < 57): bits of the word outside [moff, moff + k) are 0.
+__device__ __forceinline__ uint32_t item_word_general(const uint32_t* w, uint64_t head, uint32_t off, uint32_t k,
+                                                      uint32_t moff, uint32_t mw) {
+  const uint32_t d0 = max(32u * mw, moff) - moff;
+  const uint32_t d1 = min(32u * mw + 32u, moff + k) - moff;
+  const uint32_t sh = moff + d0 - 32u * mw;  // bit of the word that receives d0
+  uint32_t v = 0;
+  if (d0 < 57u) {
+    const uint32_t e = min(d1, 57u);
+    v = (static_cast<uint32_t>(head >> d0) & low_mask(e - d0)) << sh;
+  }
+  if (d1 > 57u) {
+    const uint32_t dd = max(d0, 57u);
+    const uint32_t j = run_of(dd);
+    const uint32_t nb = min(32u, (2u << j) - j - 2 - dd);  // bits before the next run starts
+    const uint32_t src = off + kPadBits + dd + j + 1;
+    const uint32_t x0 = sm_bits32(w, src), x1 = sm_bits32(w, src + 1);
+    const uint32_t part = ((x0 & low_mask(nb)) | (x1 & ~low_mask(nb))) & low_mask(d1 - dd);
+    v |= part << (sh + dd - d0);
+  }
+  return v;
+}
+
 // Redundancy removal + merger for one item by its group: lane q builds message
 // words mw0 + q, mw0 + q + L, ...  Data index d sits in run j at buffer bit
 // off + kPadBits + d + j + 1.  d < 57 comes from rr_head57; from d = 57 on
 // every run is >= 63 bits long, so a 32-bit window holds at most one run
-// boundary: the word is two funnel-shifted slices one bit apart, merged at the
-// boundary -- branch free.  Words wholly inside the item are stored, the
-// item's edge words (shared with neighbours) OR-ed atomically.  fb = message
-// bit to flip (the corrected data bit) or ~0.
+// boundary: an interior word is two funnel-shifted slices one bit apart,
+// merged at the boundary (branch free, the run tracked incrementally per
+// lane).  Interior words are stored; the item's edge words (shared with
+// neighbours) and the words holding d < 57 take the general path and are
+// OR-ed atomically.  fb = message bit to flip (the corrected data bit) or ~0.
 __device__ __forceinline__ void group_rr(const uint32_t* w, uint32_t* mbuf, uint32_t off, uint32_t k,
                                          uint32_t moff, uint32_t fb, uint32_t q, uint32_t L) {
   const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
+  // interior words: wholly inside the item and wholly at d >= 57
+  const uint32_t ia = max((moff + 57 + 31) / 32, (moff + 31) / 32), ib = (moff + k) / 32;
   uint64_t head = 0;
-  const bool need_head = q < 3;  // the words holding d < 57 are the first (at most) three
-  if (need_head) head = rr_head57(w, off);
-  for (uint32_t mw = mw0 + q; mw < mw1; mw += L) {
-    const uint32_t d0 = max(32u * mw, moff) - moff;
-    const uint32_t d1 = min(32u * mw + 32u, moff + k) - moff;
-    const uint32_t sh = moff + d0 - 32u * mw;  // bit of the word that receives d0
-    uint32_t v = 0;
-    if (d0 < 57u) {
-      const uint32_t e = min(d1, 57u);
-      v = (static_cast<uint32_t>(head >> d0) & low_mask(e - d0)) << sh;
-    }
-    if (d1 > 57u) {
-      const uint32_t dd = max(d0, 57u);
-      const uint32_t j = run_of(dd);
-      const uint32_t nb = min(32u, (2u << j) - j - 2 - dd);  // bits before the next run starts
-      const uint32_t src = off + kPadBits + dd + j + 1;
-      const uint32_t x0 = sm_bits32(w, src), x1 = sm_bits32(w, src + 1);
-      const uint32_t part = ((x0 & low_mask(nb)) | (x1 & ~low_mask(nb))) & low_mask(d1 - dd);
-      v |= part << (sh + dd - d0);
-    }
+  if (q < 3) head = rr_head57(w, off);  // the words holding d < 57 are the first (at most) three
+  // general words: the head [mw0, min(ia, mw1)) and the tail [max(ib, ia), mw1) -- a few each
+  const bool has_interior = ia < ib;
+  const uint32_t he = has_interior ? ia : mw1, ts = has_interior ? ib : mw1;
+  for (uint32_t i = q; i < (he - mw0) + (mw1 - ts); i += L) {
+    const uint32_t mw = (i < he - mw0) ? mw0 + i : ts + (i - (he - mw0));
+    uint32_t v = item_word_general(w, head, off, k, moff, mw);
     if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
-    if (32 * mw >= moff && 32 * mw + 32 <= moff + k) mbuf[mw] = v;
-    else atomicOr(&mbuf[mw], v);
+    atomicOr(&mbuf[mw], v);
+  }
+  // interior words, lane q: ia + q', ia + q' + L, ... with q' the lane's slot in that sequence
+  uint32_t mw = ia + ((q + L - (ia - mw0) % L) % L);
+  if (has_interior && mw < ib) {
+    uint32_t dd = 32u * mw - moff;
+    uint32_t j = run_of(dd);
+    uint32_t nxt = (2u << j) - j - 2;   // first data index of run j + 1
+    const uint32_t base = off + kPadBits + 1;
+    for (; mw < ib; mw += L, dd += 32u * L) {
+      while (dd >= nxt) {
+        ++j;
+        nxt = (2u << j) - j - 2;
+      }
+      const uint32_t src = base + dd + j;
+      const uint32_t qw = src >> 5, r = src & 31u;
+      const uint32_t a0 = w[qw], a1 = w[qw + 1];
+      const uint32_t x0 = __funnelshift_r(a0, a1, r);                          // run j
+      const uint32_t x1 = (r == 31u) ? a1 : __funnelshift_r(a0, a1, r + 1);   // run j + 1: one bit later
+      const uint32_t lm = low_mask(min(32u, nxt - dd));
+      uint32_t v = (x0 & lm) | (x1 & ~lm);
+      if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
+      mbuf[mw] = v;
+    }
   }
 }
 
