@@ -38,6 +38,8 @@
 //
 // Nothing here is shared with oracle/ (the CPU checker).
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -46,6 +48,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "hamming.h"
 
@@ -112,6 +115,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+// 2-D TMA (tensor map, e.g. 128-byte swizzled): global -> shared.
+__device__ __forceinline__ void tensor_g2s_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tensor_g2s_3d(void* dst, const void* tmap, int x, int y, int z, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
 // 1-D TMA: shared -> global, bulk-group completion.
@@ -295,6 +315,20 @@ __device__ __forceinline__ void put_codeword(uint32_t (&o)[NO], int b, uint32_t 
 // f4, reading R17), codeword c = bits [c 2^m, (c+1) 2^m) with bit 0 the
 // overall parity -- register bit p is position p in both cases (bit 0 is the
 // dummy resp. the parity bit), so a2..a5 are shared.
+// Shared-memory 16-byte unit of tile unit g (stream order) for tiles loaded
+// by the swizzled tensor map, lanes owning IN_W words each.  The map views
+// the tile as 128-byte rows; with RPL = IN_W / 32 >= 2 rows per lane it is
+// 3-D and lands row h of lane l at smem row r = h * 32 + l (so the 8 lanes of
+// a 128-bit access phase sit in 8 different rows), otherwise r = the stream
+// row.  CU_TENSOR_MAP_SWIZZLE_128B then puts unit c of row r at c ^ (r & 7).
+template <int IN_W>
+__host__ __device__ __forceinline__ constexpr uint32_t swz_unit(uint32_t g) {
+  constexpr uint32_t RPL = IN_W / 32;
+  const uint32_t row = g >> 3;
+  const uint32_t r = (RPL >= 2) ? (row % RPL) * 32 + row / RPL : row;
+  return r * 8 + ((g ^ r) & 7u);
+}
+
 template <int M, bool EXT = false>
 struct DecodeOp {
   static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
@@ -304,7 +338,16 @@ struct DecodeOp {
   static constexpr bool HAS_SIDE = true;
   static constexpr int NCOUNT = EXT ? 2 : 1;
   static constexpr int SHARED = 0;  // CTA-shared bytes (lookup tables)
-  struct Args {};
+  // SECDED lanes own 2^m words: a power-of-two stride would put all lanes'
+  // reads of their own codewords in the same banks, so SECDED tiles are
+  // loaded by a TMA tensor map with the 128-byte swizzle and read back
+  // through swz_unit (below).
+  static constexpr bool SWZ = EXT;
+  struct NoArgs {};
+  struct TmapArgs {
+    CUtensorMap tmap;  // the input as rows of 128 bytes, box = one tile
+  };
+  using Args = typename std::conditional<EXT, TmapArgs, NoArgs>::type;
   __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
   // counts from the side bytes: perfect code -- nonzero syndromes; SECDED --
   // [corrected (bit 6), double errors detected (bit 7)]
@@ -330,8 +373,21 @@ struct DecodeOp {
                                                   const Args&, const uint8_t* /*sh*/) {
     constexpr int n = Geo<M>::n, k = Geo<M>::k;
     uint32_t w[IN_W];
+    if constexpr (SWZ) {  // `in` is the tile base; this lane's 16-byte units through the swizzle
+      constexpr int CPL = IN_W / 4;
+      const uint32_t l = threadIdx.x & 31u;
 #pragma unroll
-    for (int i = 0; i < IN_W; ++i) w[i] = in[i];
+      for (int u = 0; u < CPL; ++u) {
+        const uint4 v = reinterpret_cast<const uint4*>(in)[swz_unit<IN_W>(l * CPL + u)];
+        w[4 * u] = v.x;
+        w[4 * u + 1] = v.y;
+        w[4 * u + 2] = v.z;
+        w[4 * u + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < IN_W; ++i) w[i] = in[i];
+    }
     __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     uint32_t o[k];
 #pragma unroll
@@ -717,11 +773,43 @@ struct GenerateOp {
   }
 };
 // ------------------------------------------------------------------ kernels
+template <class Op, class = void>
+struct Swizzled {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct Swizzled<Op, decltype(void(Op::SWZ))> {
+  static constexpr bool value = Op::SWZ;
+};
+
 template <class Op>
 struct TileBytes {
   static constexpr int IN = Op::IN_W * 128;   // 32 lanes x IN_W words x 4 B
   static constexpr int OUT = Op::OUT_W * 128;
+  static constexpr bool SWZ = Swizzled<Op>::value;
+  // shared-memory byte offset of tile byte i (128-byte swizzle for SWZ tiles)
+  __host__ __device__ static constexpr uint32_t staged(uint32_t i) {
+    if constexpr (SWZ) {
+      return (swz_unit<Op::IN_W>(i >> 4) << 4) | (i & 15u);
+    } else {
+      return i;
+    }
+  }
 };
+
+// Issue the TMA load of one input tile into a stage.
+template <class Op>
+__device__ __forceinline__ void load_tile(uint8_t* stage, const uint8_t* in, uint64_t t, uint64_t* bar,
+                                          const typename Op::Args& args, uint64_t pol) {
+  constexpr int IN = TileBytes<Op>::IN;
+  mbar_arrive_expect_tx(bar, IN);
+  if constexpr (TileBytes<Op>::SWZ) {
+    if constexpr (Op::IN_W / 32 >= 2) tensor_g2s_3d(stage, &args.tmap, 0, static_cast<int>(t * 32), 0, bar, pol);
+    else tensor_g2s_2d(stage, &args.tmap, 0, static_cast<int>(t * (IN / 128)), bar, pol);
+  } else {
+    bulk_g2s(stage, in + t * IN, IN, bar, pol);
+  }
+}
 
 // The ragged last tile (rem < 1024 codewords) of a launch: bounded 16-byte
 // loads with zero fill, input pad bits past rem codewords cleared, the same
@@ -736,11 +824,13 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
   if constexpr (IN > 0) {
     const uint64_t ib0 = tile * IN;
     const uint64_t nb = in_total - ib0;  // bytes of this tile that exist (< IN)
-    for (int i = lane * 16; i < IN; i += 512) {
+    using TB = TileBytes<Op>;
+    for (int i = lane * 16; i < IN; i += 512) {  // 16-byte units, placed as the TMA would place them
+      uint8_t* dst = ibuf + TB::staged(i);
       if (static_cast<uint64_t>(i) + 16 <= nb) {
-        *reinterpret_cast<uint4*>(ibuf + i) = *reinterpret_cast<const uint4*>(in + ib0 + i);
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(in + ib0 + i);
       } else {
-        for (int b = 0; b < 16; ++b) ibuf[i + b] = (static_cast<uint64_t>(i + b) < nb) ? in[ib0 + i + b] : 0;
+        for (int b = 0; b < 16; ++b) dst[b] = (static_cast<uint64_t>(i + b) < nb) ? in[ib0 + i + b] : 0;
       }
     }
     __syncwarp();
@@ -748,15 +838,16 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
     uint32_t* iw = reinterpret_cast<uint32_t*>(ibuf);
     for (int i = lane; i < IN / 4; i += 32) {
       const uint64_t b = static_cast<uint64_t>(i) * 32;
-      if (b >= vbits) iw[i] = 0;
-      else if (b + 32 > vbits) iw[i] &= (1u << (vbits - b)) - 1u;
+      uint32_t& x = iw[TB::staged(4u * i) / 4];
+      if (b >= vbits) x = 0;
+      else if (b + 32 > vbits) x &= (1u << (vbits - b)) - 1u;
     }
     __syncwarp();
   }
   const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
   uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  Op::lane(reinterpret_cast<const uint32_t*>(ibuf) + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew,
-           tile * kTileCw + lane * 32, valid, args, sh);
+  Op::lane(reinterpret_cast<const uint32_t*>(ibuf) + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W),
+           obuf + lane * Op::OUT_W, sidew, tile * kTileCw + lane * 32, valid, args, sh);
   __syncwarp();
   const uint64_t ob0 = tile * OUT;
   const uint64_t nbo = out_total - ob0;
@@ -794,14 +885,18 @@ struct TileLayout {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   static constexpr bool IN_PLACE = WANT_IN_PLACE && IN > 0 && OUT <= IN;
   static constexpr int OUT_BUFS = IN_PLACE ? 0 : 2;
-  __host__ __device__ static constexpr int warp_bytes(int stages) { return stages * IN + OUT_BUFS * OUT; }
+  // swizzled stages stay 1024-byte aligned from warp to warp
+  __host__ __device__ static constexpr int warp_bytes(int stages) {
+    return TileBytes<Op>::SWZ ? (stages * IN + OUT_BUFS * OUT + 1023) / 1024 * 1024 : stages * IN + OUT_BUFS * OUT;
+  }
 };
 
 template <class Op, int WARPS, int STAGES, bool INPLACE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
                  uint64_t n_full, uint32_t rem, uint64_t in_total, uint64_t out_total,
-                 unsigned long long* __restrict__ counter, int store_count, typename Op::Args args) {
+                 unsigned long long* __restrict__ counter, int store_count,
+                 const __grid_constant__ typename Op::Args args) {
   using TL = TileLayout<Op, INPLACE>;
   constexpr int IN = TL::IN, OUT = TL::OUT;
   constexpr int WARP_SMEM = TL::warp_bytes(STAGES);
@@ -810,8 +905,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* const sh = smem;  // Op::SHARED bytes of CTA-wide tables first
-  uint8_t* wbase = smem + Op::SHARED + warp * WARP_SMEM;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Op::SHARED + WARPS * WARP_SMEM) + warp * STAGES;
+  // 128-byte-swizzled TMA destinations must be 1024-byte aligned
+  uint8_t* const tiles = smem + Op::SHARED +
+                         (TileBytes<Op>::SWZ ? ((1024u - (smem_addr(smem + Op::SHARED) & 1023u)) & 1023u) : 0u);
+  uint8_t* wbase = tiles + warp * WARP_SMEM;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tiles + WARPS * WARP_SMEM) + warp * STAGES;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
@@ -829,10 +927,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) {
         const uint64_t t = gw + s * nw;
-        if (t < n_full) {
-          mbar_arrive_expect_tx(&bars[s], IN);
-          bulk_g2s(wbase + s * IN, in + t * IN, IN, &bars[s], pol);
-        }
+        if (t < n_full) load_tile<Op>(wbase + s * IN, in, t, &bars[s], args, pol);
       }
     }
     __syncwarp();
@@ -854,7 +949,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
     uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
-    Op::lane(ibuf + lane * Op::IN_W, obuf + lane * Op::OUT_W, sidew, t * kTileCw + lane * 32, 32, args, sh);
+    Op::lane(ibuf + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W), obuf + lane * Op::OUT_W, sidew,
+             t * kTileCw + lane * 32, 32, args, sh);
     fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
     __syncwarp();
     if (lane == 0) {
@@ -868,17 +964,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
           if (nt < n_full) {
             const int ps = static_cast<int>((it - 1) % STAGES);
             bulk_wait_read<1>();
-            mbar_arrive_expect_tx(&bars[ps], IN);
-            bulk_g2s(wbase + ps * IN, in + nt * IN, IN, &bars[ps], pol);
+            load_tile<Op>(wbase + ps * IN, in, nt, &bars[ps], args, pol);
           }
         }
       }
       if constexpr (!TL::IN_PLACE && IN > 0) {
         const uint64_t nt = t + STAGES * nw;
-        if (nt < n_full) {
-          mbar_arrive_expect_tx(&bars[st], IN);
-          bulk_g2s(wbase + st * IN, in + nt * IN, IN, &bars[st], pol);
-        }
+        if (nt < n_full) load_tile<Op>(wbase + st * IN, in, nt, &bars[st], args, pol);
       }
     }
     if constexpr (Op::HAS_SIDE) {
@@ -945,8 +1037,9 @@ int sm_count(int dev) {
 template <class Op, int WARPS, int STAGES, bool INPLACE = true>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
-  static constexpr size_t SMEM =
-      Op::SHARED + static_cast<size_t>(WARPS) * TileLayout<Op, INPLACE>::warp_bytes(STAGES) + WARPS * STAGES * 8;
+  static constexpr size_t SMEM = Op::SHARED + (TileBytes<Op>::SWZ ? 1024 : 0) +
+                                 static_cast<size_t>(WARPS) * TileLayout<Op, INPLACE>::warp_bytes(STAGES) +
+                                 WARPS * STAGES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
   static hamming_status run(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t n_cw, uint64_t in_total,
@@ -1004,6 +1097,55 @@ template <> struct Shape<3> { static constexpr int W = 16, S = 4; };
 template <> struct Shape<4> { static constexpr int W = 16, S = 4; };
 template <> struct Shape<5> { static constexpr int W = 12, S = 3; };
 template <> struct Shape<6> { static constexpr int W = 7, S = 2; };
+
+// The 2-D, 128-byte-swizzled tensor map over the full tiles of a SECDED input
+// (rows of 128 bytes, one box = one tile of `tile_bytes`).  The driver entry
+// point is resolved once through the runtime (no -lcuda).
+hamming_status make_tile_tmap(CUtensorMap* map, const void* base, uint64_t n_full, int tile_bytes) {
+  memset(map, 0, sizeof(*map));
+  if (n_full == 0) return HAMMING_OK;  // no TMA loads: the tail loader handles everything
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (encode == nullptr) return set_err(HAMMING_E_CUDA, "cuTensorMapEncodeTiled entry point not found");
+  const uint64_t rows = n_full * static_cast<uint64_t>(tile_bytes / 128);
+  if (rows > (1ull << 31)) return set_err(HAMMING_E_RANGE, "input too large for one tensor map");
+  const cuuint32_t rpl = static_cast<cuuint32_t>(tile_bytes / (32 * 128));  // 128-byte rows per lane
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r;
+  if (rpl >= 2) {  // {byte, lane, row of the lane}: smem box order [row of lane][lane][128 B]
+    const cuuint64_t dims[3] = {128, rows / rpl, rpl};
+    const cuuint64_t strides[2] = {128ull * rpl, 128};
+    const cuuint32_t box[3] = {128, 32, rpl};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[2] = {128, rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(tile_bytes / 128)};
+    r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return set_err(HAMMING_E_CUDA, "cuTensorMapEncodeTiled failed");
+  return HAMMING_OK;
+}
+
+template <class Op, int WARPS, int STAGES>
+hamming_status run_swizzled(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t N, uint64_t ib, uint64_t ob,
+                            unsigned long long* counter, cudaStream_t st) {
+  typename Op::Args a;
+  const hamming_status s = make_tile_tmap(&a.tmap, in, N / kTileCw, TileBytes<Op>::IN);
+  if (s != HAMMING_OK) return s;
+  return Launcher<Op, WARPS, STAGES, true>::run(in, out, side, N, ib, ob, counter, a, st);
+}
 
 bool ranges_overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
   if (!a || !b || !na || !nb) return false;
@@ -1378,7 +1520,7 @@ hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void
     switch (m) {
 #define HAMMING_SECDED_SMALL(MM) \
   case MM:                       \
-    return Launcher<DecodeOp<MM, true>, 4, 2, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+    return run_swizzled<DecodeOp<MM, true>, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
       HAMMING_SECDED_SMALL(3)
       HAMMING_SECDED_SMALL(4)
       HAMMING_SECDED_SMALL(5)
@@ -1387,10 +1529,10 @@ hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void
     }
   }
   switch (m) {
-    case 3: return Launcher<DecodeOp<3, true>, 16, 8, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
-    case 4: return Launcher<DecodeOp<4, true>, 16, 6, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
-    case 5: return Launcher<DecodeOp<5, true>, 12, 3, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
-    case 6: return Launcher<DecodeOp<6, true>, 8, 3, true>::run(in, out, flags_dev, N, ib, ob, counts_dev, {}, st);
+    case 3: return run_swizzled<DecodeOp<3, true>, 16, 8>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 4: return run_swizzled<DecodeOp<4, true>, 16, 6>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 5: return run_swizzled<DecodeOp<5, true>, 12, 3>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 6: return run_swizzled<DecodeOp<6, true>, 8, 3>(in, out, flags_dev, N, ib, ob, counts_dev, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_decode_secded: m must be in [3, 6]");
 }
