@@ -259,25 +259,95 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
 }
 
 // ---------------------------------------------------------------------------
-// Decode engine for long (shortened) codewords: a warp stages a BATCH of
-// consecutive packets (TMA bulk, double-buffered) and decodes its items -- the
-// (packet, segment) codewords -- with GROUPS of L lanes per item (L a power
-// of two chosen from the codeword length: short segments take one or two
-// lanes each, an 8013-bit segment takes the whole warp).  Within a group the
-// chunks of the syndrome and the words of the message are dealt round-robin;
-// the group XOR-reduces with L-1 shuffles.  Message words wholly inside an
-// item are stored, words shared with a neighbouring item are OR-ed atomically
-// into the batch's shared message buffer, which the warp then writes out.
+// Packet decode.  A warp stages a BATCH of G consecutive packets in shared
+// memory (TMA bulk, double-buffered) and decodes it in three passes:
+//   R  (redundancy removal + merger) -- one lane per 32-bit
+//      message word.  The geometry is the same for every packet, so the host
+//      precomputes, per message word, where its bits sit in the packet stream
+//      as "pieces": maximal slices that stay inside one run (positions
+//      2^j+1 .. 2^(j+1)-1) of one segment.  From data index 57 on a run is
+//      >= 63 bits long, so almost every word is one or two slices: two funnel
+//      shifts and one merge.  The few words near a segment head (data index
+//      < 57: runs of 1, 3, 7, 15, 31 bits) or across a segment boundary are
+//   H  ("head" words) built by one lane each from their piece list;
+//   S  (syndrome, the checksum vector) -- per (packet, segment) item,
+//      by a group of L lanes: s = XOR_j [32 j * parity(x_j)] ^ S5(XOR_j x_j);
+//      a correctable s flips the corrected data bit of the message in place.
+// Every message word is written exactly once (R or H), so nothing is zeroed.
 // ---------------------------------------------------------------------------
+constexpr uint32_t kPktMaxWords = kPktMaxMsgBytes / 4;
+constexpr uint32_t kPktMaxSpecial = 80;   // <= 57 t / 32 + 2 t + 1 head words
+constexpr uint32_t kPktMaxPieces = 640;
+
+struct PacketTables {
+  uint32_t Wp;                    // message words per packet, ceil(msg_bytes / 4)
+  uint32_t n_special, n_pieces;
+  uint32_t mag_t, mag_ns, mag_wp; // floor(2^32 / d) for d = t, n_special, Wp (divmod_small)
+  // src0 (bits 0..15) | nb0 (bits 16..21): a word is slice 0 (nb0 bits) and, if nb0 < 32, slice 1 =
+  // the stream one bit after slice 0 ends (a skipped parity position); head words: 32 << 16
+  uint32_t word0[kPktMaxWords];
+  uint32_t special[kPktMaxSpecial + 1];  // word index | first piece << 16; [n_special]: end
+  uint32_t piece[kPktMaxPieces];         // src (bits 0..15) | len (16..21) | pos (24..28)
+};
+// src = bit of the packet stream (from its first bit) holding the slice's first data bit.
+
+// host: data index -> run j (data indices of run j: 2^j-j-1 .. 2^(j+1)-j-3)
+uint32_t host_run_of(uint32_t d) {
+  uint32_t j = 1;
+  while (d >= (2u << j) - j - 2) ++j;
+  return j;
+}
+
+hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
+  const uint32_t bits = g.msg_bytes * 8u;
+  T.Wp = (g.msg_bytes + 3) / 4;
+  T.n_special = 0;
+  T.n_pieces = 0;
+  uint32_t seg = 0;
+  for (uint32_t W = 0; W < T.Wp; ++W) {
+    uint32_t src[32], len[32], pos[32], np = 0;
+    uint32_t d = 32u * W;
+    const uint32_t dend = std::min(32u * W + 32u, bits);
+    while (d < dend) {
+      while (d >= g.moff[seg] + g.k[seg]) ++seg;
+      const uint32_t dl = d - g.moff[seg];
+      const uint32_t j = host_run_of(dl);
+      const uint32_t run_end = std::min((2u << j) - j - 2, g.k[seg]);
+      const uint32_t take = std::min(run_end - dl, dend - d);
+      src[np] = g.off[seg] + dl + j + 1;  // position dl + j + 2 is packet bit off + position - 1
+      len[np] = take;
+      pos[np] = d - 32u * W;
+      ++np;
+      d += take;
+    }
+    if (np == 1 || (np == 2 && src[1] == src[0] + len[0] + 1)) {  // slice 1 = the stream one bit later
+      T.word0[W] = src[0] | (len[0] << 16);
+    } else {
+      if (T.n_special >= kPktMaxSpecial || T.n_pieces + np > kPktMaxPieces)
+        return set_err(HAMMING_E_ARG, "packets: piece table overflow");
+      T.word0[W] = 32u << 16;  // a harmless one-slice read, overwritten by pass H
+      T.special[T.n_special++] = W | (T.n_pieces << 16);
+      for (uint32_t i = 0; i < np; ++i) T.piece[T.n_pieces++] = src[i] | (len[i] << 16) | (pos[i] << 24);
+    }
+  }
+  T.special[T.n_special] = T.n_pieces << 16;
+  auto mag = [](uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : static_cast<uint32_t>((1ull << 32) / d); };
+  T.mag_t = mag(g.t);
+  T.mag_ns = mag(T.n_special);
+  T.mag_wp = mag(T.Wp);
+  return HAMMING_OK;
+}
+
 struct BatchGeom {
   uint32_t G;          // packets per batch
-  uint32_t L;          // lanes per item (power of two)
+  uint32_t L;          // lanes per item in pass S (power of two)
   uint32_t in_cap;     // bytes per input buffer: 16 pad + G*stride + 16 slack
-  uint32_t msg_cap;    // bytes of the message buffer (16-aligned, + slack)
-  uint32_t warp_bytes; // 2*in_cap + msg_cap + 16*G (status words)
+  uint32_t msg_cap;    // bytes of the message buffer: G packets of Wp words (+ slack)
+  uint32_t warp_bytes; // 2*in_cap + msg_cap + status words
+  uint32_t tab_bytes;  // CTA tables in front of the warp areas
 };
 
-hamming_status batch_geom(const PacketGeom& g, uint64_t stride, BatchGeom& b) {
+hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
   const uint32_t chunks = (maxn + 32) / 32;
@@ -287,15 +357,17 @@ hamming_status batch_geom(const PacketGeom& g, uint64_t stride, BatchGeom& b) {
 #define HAM_PKT_BUDGET (10 * 1024)
 #endif
   const uint64_t budget = HAM_PKT_BUDGET;  // shared bytes per warp (tuned: tools/tune_shapes.py packets)
-  const uint64_t per = 2 * stride + (g.msg_bytes + 3) / 4 * 4 + 4;
+  const uint64_t per = 2 * stride + 4ull * T.Wp + 4;
   uint64_t G = budget > 96 ? (budget - 96) / per : 1;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
   b.G = static_cast<uint32_t>(G);
   b.L = L;
   b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
-  b.msg_cap = static_cast<uint32_t>((G * g.msg_bytes + 15) / 16 * 16 + 16);
+  b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
   b.warp_bytes = 2 * b.in_cap + b.msg_cap + static_cast<uint32_t>(16 * ((G * 4 + 15) / 16));
-  if (b.warp_bytes * 2ull > 227ull * 1024) return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
+  b.tab_bytes = (16 * T.Wp + 4 * (kPktMaxSpecial + 1) + 4 * T.n_pieces + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
+  if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
+    return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
   return HAMMING_OK;
 }
 
@@ -325,9 +397,72 @@ __device__ __forceinline__ uint32_t group_syndrome(const uint32_t* w, uint32_t o
       P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
     }
   }
-  for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
-    X ^= __shfl_xor_sync(0xffffffffu, X, sh);
-    P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+  if (L == 32) {  // one REDUX each for a whole-warp item
+    X = __reduce_xor_sync(0xffffffffu, X);
+    P = __reduce_xor_sync(0xffffffffu, P);
+  } else {
+    for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
+      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+    }
+  }
+  return P ^ xor_of_indices(X);
+}
+
+// The same syndrome with L a compile-time group size and no per-chunk POPC.
+// Lane q takes chunks j = q + L m, m = 8 blk + it (it < 8, unrolled), over
+// j = 0 .. C-2 unmasked (position 0 sits in chunk 0, which contributes 0 to
+// both halves of s whatever its bits), and the group's rank-0 lane adds the
+// last chunk masked to positions <= n.  The high part XOR_j [32 j par(x_j)]
+// is rebuilt at the end from parities of a few accumulators: with q < L a
+// power of two, j = q | (L m), so XOR over odd-parity chunks of j is
+// q*par(X) ^ L*(8*BB ^ par(A0) ^ 2 par(A1) ^ 4 par(A2)), where A_b is the XOR
+// of the chunks whose `it` has bit b and BB the XOR of the block indices with
+// an odd block parity.
+template <uint32_t L>
+__device__ __forceinline__ uint32_t group_syndrome_l(const uint32_t* w, uint32_t off, uint32_t n, bool active,
+                                                     uint32_t q) {
+  const uint32_t C = active ? (n + 32) / 32 : 0;
+  const uint32_t o = off + kPadBits - 1;
+  const uint32_t* wq = w + (o >> 5) + q;
+  const uint32_t rb = o & 31u;
+  uint32_t X = 0, A0 = 0, A1 = 0, A2 = 0, BB = 0;
+  const uint32_t interior = C > 0 ? C - 1 : 0;  // chunks 0 .. C-2
+  for (uint32_t blk = 0; 8 * L * blk < interior; ++blk) {
+    const uint32_t* wb = wq + 8 * L * blk;
+    // chunks of this lane in the block: j = q + 8 L blk + L it < interior
+    const int cnt = static_cast<int>(interior - 8 * L * blk) - static_cast<int>(q);
+    uint32_t Xb = 0;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      if (static_cast<int>(L) * it < cnt) {
+        const uint32_t x = __funnelshift_r(wb[L * it], wb[L * it + 1], rb);
+        Xb ^= x;
+        if (it & 1) A0 ^= x;
+        if (it & 2) A1 ^= x;
+        if (it & 4) A2 ^= x;
+      }
+    }
+    X ^= Xb;
+    BB ^= (__popc(Xb) & 1u) ? blk : 0u;
+  }
+  uint32_t P = 32u * ((q * (__popc(X) & 1u)) ^
+                      L * ((8u * BB) ^ (__popc(A0) & 1u) ^ ((__popc(A1) & 1u) << 1) ^ ((__popc(A2) & 1u) << 2)));
+  if (active && q == 0) {  // the last chunk, positions past n masked off
+    const uint32_t j = C - 1;
+    const uint32_t x = __funnelshift_r(w[(o >> 5) + j], w[(o >> 5) + j + 1], rb) & low_mask(n - 32 * j + 1);
+    X ^= x;
+    P ^= (__popc(x) & 1u) ? 32u * j : 0u;
+  }
+  if constexpr (L == 32) {
+    X = __reduce_xor_sync(0xffffffffu, X);
+    P = __reduce_xor_sync(0xffffffffu, P);
+  } else {
+#pragma unroll
+    for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
+      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+    }
   }
   return P ^ xor_of_indices(X);
 }
@@ -421,14 +556,46 @@ __device__ __forceinline__ void group_rr(const uint32_t* w, uint32_t* mbuf, uint
   }
 }
 
+// q = u / d, r = u % d from mag = floor(2^32 / d) (2^32 - 1 for d = 1): the
+// estimate is q or q - 1, one correction step.
+__device__ __forceinline__ uint32_t divmod_small(uint32_t u, uint32_t d, uint32_t mag, uint32_t& r) {
+  uint32_t q = __umulhi(u, mag);
+  r = u - q * d;
+  if (r >= d) {
+    ++q;
+    r -= d;
+  }
+  return q;
+}
+
+template <uint32_t L>
 __global__ void __launch_bounds__(kPktWarps * 32)
     packets_decode_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ BatchGeom bg,
-                          const __grid_constant__ PacketArgs a) {
+                          const __grid_constant__ PacketArgs a, const __grid_constant__ PacketTables T) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_counts[2];
   __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* wb = smem + warp * bg.warp_bytes;
+  const uint32_t Wp = T.Wp, ns = T.n_special;
+  // CTA tables: word descriptors {word of slice 0, word of slice 1, shifts, nb},
+  // head words, pieces, per-segment geometry
+  uint4* wdesc = reinterpret_cast<uint4*>(smem);
+  uint32_t* spec = reinterpret_cast<uint32_t*>(smem + 16 * Wp);
+  uint32_t* pieces = spec + kPktMaxSpecial + 1;
+  uint32_t* sg = pieces + T.n_pieces;  // [off | n | k | moff] x kPktMaxSeg
+  for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
+    const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
+    wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, 0u);
+  }
+  for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) spec[i] = T.special[i];
+  for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = T.piece[i];
+  if (threadIdx.x < g.t) {
+    sg[threadIdx.x] = g.off[threadIdx.x];
+    sg[kPktMaxSeg + threadIdx.x] = g.n[threadIdx.x];
+    sg[2 * kPktMaxSeg + threadIdx.x] = g.k[threadIdx.x];
+    sg[3 * kPktMaxSeg + threadIdx.x] = g.moff[threadIdx.x];
+  }
+  uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
   uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap);
   uint32_t* pst = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + bg.msg_cap);  // per-packet status
   uint64_t* bars = bars_all + warp * 2;
@@ -438,9 +605,9 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
   const uint64_t pol = policy_evict_first();
-  const uint32_t L = bg.L, q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
+  const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
   const uint32_t groups = 32 / L;
-  const uint32_t msg_bits = g.msg_bytes * 8;
+  const uint32_t stride_bits = static_cast<uint32_t>(a.in_stride * 8);
   uint32_t n_corr = 0, n_fail = 0;
   auto batch_bytes = [&](uint64_t b) -> uint32_t {
     const uint64_t p0 = b * bg.G;
@@ -467,33 +634,68 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     const uint64_t p0 = b * bg.G;
     const uint64_t left = a.n_packets - p0;
     const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
-    const uint32_t items = np * g.t;
-    const uint32_t mwords = (np * g.msg_bytes + 3) / 4;
-    for (uint32_t i = lane; i < mwords; i += 32) mbuf[i] = 0;
     for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
     mbar_wait(&bars[buf], (it >> 1) & 1u);
     __syncwarp();
-    for (uint32_t base = 0; base < items; base += groups) {
-      const uint32_t item = base + gid;
-      const bool active = item < items;
-      const uint32_t pk = active ? item / g.t : 0, seg = active ? item % g.t : 0;
-      const uint32_t off = static_cast<uint32_t>(pk * a.in_stride * 8) + g.off[seg];
-      const uint32_t n = g.n[seg], k = g.k[seg];
-      const uint32_t moff = pk * msg_bits + g.moff[seg];
-      const uint32_t s = group_syndrome(w, off, n, active, q, L);
-      if (!active) continue;
-      const bool corr = s != 0 && s <= n;
-      const bool fail = s > n;
-      // data index of the corrected position (none for a parity position or no correction)
-      uint32_t ds = 0xFFFFFFFFu;
-      if (corr && (s & (s - 1)) != 0) ds = s - (31u - __clz(s)) - 2;
-      if (q == 0) {
-        if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
-        if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
-        n_corr += corr;
-        n_fail += fail;
+    {  // pass R: every word as one or two slices (head words are rewritten by pass H)
+      const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
+      uint32_t p = 0, W = lane;
+      if (W >= Wp) p = divmod_small(W, Wp, T.mag_wp, W);
+      const uint32_t total = np * Wp;
+      for (uint32_t u = lane; u < total; u += 32) {
+        const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, -}
+        const uint32_t* wp = w + 4 + p * wstride + d.x;  // (after the 16-byte pad)
+        const uint32_t a0 = wp[0], a1 = wp[1];
+        // slice 1 is the stream one bit further on (the parity position skipped)
+        mbuf[u] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+        W += 32;
+        if (W >= Wp) {
+          W -= Wp;
+          ++p;
+          if (W >= Wp) p += divmod_small(W, Wp, T.mag_wp, W);  // only when Wp < 32
+        }
       }
-      group_rr(w, mbuf, off, k, moff, ds == 0xFFFFFFFFu ? 0xFFFFFFFFu : moff + ds, q, L);
+    }
+    __syncwarp();
+    if (ns > 0) {  // pass H: head words from their piece lists
+      for (uint32_t e = lane; e < np * ns; e += 32) {
+        uint32_t i;
+        const uint32_t p = divmod_small(e, ns, T.mag_ns, i);
+        const uint32_t sp = spec[i], pe = spec[i + 1] >> 16;
+        const uint32_t base = kPadBits + p * stride_bits;
+        uint32_t v = 0;
+        for (uint32_t c = sp >> 16; c < pe; ++c) {
+          const uint32_t pc = pieces[c];
+          const uint32_t s0 = base + (pc & 0xFFFFu), len = (pc >> 16) & 63u;
+          const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
+          v |= x << ((pc >> 24) & 31u);
+        }
+        mbuf[p * Wp + (sp & 0xFFFFu)] = v;
+      }
+    }
+    __syncwarp();
+    {  // pass S: syndromes; a correctable error flips its data bit in the message
+      const uint32_t items = np * g.t;
+      for (uint32_t base = 0; base < items; base += groups) {
+        const bool active = base + gid < items;
+        uint32_t seg;
+        const uint32_t pk = divmod_small(active ? base + gid : 0, g.t, T.mag_t, seg);
+        const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
+        const uint32_t off = pk * stride_bits + sg[seg];
+        const uint32_t s = group_syndrome_l<L>(w, off, n, active, q);
+        if (active && q == 0) {
+          const bool corr = s != 0 && s <= n;
+          const bool fail = s > n;
+          if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
+          if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
+          n_corr += corr;
+          n_fail += fail;
+          if (corr && (s & (s - 1)) != 0) {  // a data position: message bit moff + s - floor(log2 s) - 2
+            const uint32_t fb = sg[3 * kPktMaxSeg + seg] + s - (31u - __clz(s)) - 2;
+            atomicXor(&mbuf[pk * Wp + (fb >> 5)], 1u << (fb & 31u));
+          }
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
@@ -503,18 +705,21 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         bulk_g2s(wb + buf * bg.in_cap + 16, a.in + nx * bg.G * a.in_stride, batch_bytes(nx), &bars[buf], pol);
       }
     }
-    // write the batch's messages and statuses
+    // write the batch's messages (packet pk at word pk * Wp of mbuf) and statuses
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
-    if (a.out_stride == g.msg_bytes && ((reinterpret_cast<uintptr_t>(a.out) | (p0 * g.msg_bytes)) & 15u) == 0) {
-      uint8_t* dst = a.out + p0 * g.msg_bytes;
-      const uint32_t nb = np * g.msg_bytes;
-      for (uint32_t i = lane; i < nb / 16; i += 32)
-        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
-      for (uint32_t i = nb / 16 * 16 + lane; i < nb; i += 32) dst[i] = mb[i];
+    const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + p0 * a.out_stride);
+    if (a.out_stride == g.msg_bytes && (g.msg_bytes & 15u) == 0 && (ob & 15u) == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(ob);
+      for (uint32_t i = lane; i < np * g.msg_bytes / 16; i += 32) dst[i] = reinterpret_cast<const uint4*>(mbuf)[i];
+    } else if ((g.msg_bytes & 3u) == 0 && (a.out_stride & 3u) == 0 && (ob & 3u) == 0) {
+      for (uint32_t pk = 0; pk < np; ++pk) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(ob + pk * a.out_stride);
+        for (uint32_t i = lane; i < Wp; i += 32) dst[i] = mbuf[pk * Wp + i];
+      }
     } else {
       for (uint32_t pk = 0; pk < np; ++pk) {
-        uint8_t* dst = a.out + (p0 + pk) * a.out_stride;
-        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * g.msg_bytes + i];
+        uint8_t* dst = reinterpret_cast<uint8_t*>(ob + pk * a.out_stride);
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * Wp * 4 + i];
       }
     }
     if (a.status != nullptr)
@@ -537,27 +742,45 @@ __global__ void __launch_bounds__(kPktWarps * 32)
 }
 
 hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, cudaStream_t st) {
+  static thread_local PacketTables T;  // rebuilt only when the geometry changes
+  static thread_local uint32_t T_msg = 0, T_t = 0;
+  if (T_msg != g.msg_bytes || T_t != g.t) {
+    T_msg = 0;
+    const hamming_status rc = build_packet_tables(g, T);
+    if (rc != HAMMING_OK) return rc;
+    T_msg = g.msg_bytes;
+    T_t = g.t;
+  }
   BatchGeom bg;
-  hamming_status rc = batch_geom(g, a.in_stride, bg);
+  hamming_status rc = batch_geom(g, T, a.in_stride, bg);
   if (rc != HAMMING_OK) return rc;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const size_t smem = static_cast<size_t>(kPktWarps) * bg.warp_bytes;
+  const size_t smem = bg.tab_bytes + static_cast<size_t>(kPktWarps) * bg.warp_bytes;
   if (smem > 227 * 1024) return set_err(HAMMING_E_ARG, "packets: shared memory budget exceeded");
-  e = cudaFuncSetAttribute(packets_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  void (*kfn)(PacketGeom, BatchGeom, PacketArgs, PacketTables) = nullptr;
+  switch (bg.L) {
+    case 1: kfn = packets_decode_kernel<1>; break;
+    case 2: kfn = packets_decode_kernel<2>; break;
+    case 4: kfn = packets_decode_kernel<4>; break;
+    case 8: kfn = packets_decode_kernel<8>; break;
+    case 16: kfn = packets_decode_kernel<16>; break;
+    default: kfn = packets_decode_kernel<32>; break;
+  }
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets decode)");
   // ask for the full shared-memory carveout so several CTAs fit per SM
-  e = cudaFuncSetAttribute(packets_decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, packets_decode_kernel, kPktWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kPktWarps * 32, smem);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets decode)");
   const uint64_t batches = (a.n_packets + bg.G - 1) / bg.G;
   const uint64_t want = (batches + kPktWarps - 1) / kPktWarps;
   const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
   if (grid > 0) {
-    packets_decode_kernel<<<grid, kPktWarps * 32, smem, st>>>(g, bg, a);
+    kfn<<<grid, kPktWarps * 32, smem, st>>>(g, bg, a, T);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "packets decode launch");
   }
