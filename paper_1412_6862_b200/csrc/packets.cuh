@@ -282,12 +282,13 @@ constexpr uint32_t kPktMaxPieces = 640;
 struct PacketTables {
   uint32_t Wp;                    // message words per packet, ceil(msg_bytes / 4)
   uint32_t n_special, n_pieces;
-  uint32_t mag_t, mag_ns, mag_wp; // floor(2^32 / d) for d = t, n_special, Wp (divmod_small)
+  uint32_t mag_t, mag_ns, mag_wp, mag_np;  // floor(2^32 / d), d = t, n_special, Wp, n_pieces (divmod_small)
   // src0 (bits 0..15) | nb0 (bits 16..21): a word is slice 0 (nb0 bits) and, if nb0 < 32, slice 1 =
   // the stream one bit after slice 0 ends (a skipped parity position); head words: 32 << 16
   uint32_t word0[kPktMaxWords];
   uint32_t special[kPktMaxSpecial + 1];  // word index | first piece << 16; [n_special]: end
   uint32_t piece[kPktMaxPieces];         // src (bits 0..15) | len (16..21) | pos (24..28)
+  uint16_t piece_word[kPktMaxPieces];    // the head word a piece belongs to
 };
 // src = bit of the packet stream (from its first bit) holding the slice's first data bit.
 
@@ -325,9 +326,12 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
     } else {
       if (T.n_special >= kPktMaxSpecial || T.n_pieces + np > kPktMaxPieces)
         return set_err(HAMMING_E_ARG, "packets: piece table overflow");
-      T.word0[W] = 32u << 16;  // a harmless one-slice read, overwritten by pass H
+      T.word0[W] = 33u << 16;  // head word: pass R writes 0, pass H ORs its pieces in
       T.special[T.n_special++] = W | (T.n_pieces << 16);
-      for (uint32_t i = 0; i < np; ++i) T.piece[T.n_pieces++] = src[i] | (len[i] << 16) | (pos[i] << 24);
+      for (uint32_t i = 0; i < np; ++i) {
+        T.piece_word[T.n_pieces] = static_cast<uint16_t>(W);
+        T.piece[T.n_pieces++] = src[i] | (len[i] << 16) | (pos[i] << 24);
+      }
     }
   }
   T.special[T.n_special] = T.n_pieces << 16;
@@ -335,6 +339,7 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
   T.mag_t = mag(g.t);
   T.mag_ns = mag(T.n_special);
   T.mag_wp = mag(T.Wp);
+  T.mag_np = mag(T.n_pieces);
   return HAMMING_OK;
 }
 
@@ -354,18 +359,19 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   uint32_t L = 1;
   while (L < 32 && L * 8 < chunks) L *= 2;
 #ifndef HAM_PKT_BUDGET
-#define HAM_PKT_BUDGET (10 * 1024)
+#define HAM_PKT_BUDGET (8 * 1024)
 #endif
   const uint64_t budget = HAM_PKT_BUDGET;  // shared bytes per warp (tuned: tools/tune_shapes.py packets)
-  const uint64_t per = 2 * stride + 4ull * T.Wp + 4;
+  const uint64_t per = 2 * stride + 8ull * T.Wp + 4;
   uint64_t G = budget > 96 ? (budget - 96) / per : 1;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
   b.G = static_cast<uint32_t>(G);
   b.L = L;
   b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
   b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
-  b.warp_bytes = 2 * b.in_cap + b.msg_cap + static_cast<uint32_t>(16 * ((G * 4 + 15) / 16));
-  b.tab_bytes = (16 * T.Wp + 4 * (kPktMaxSpecial + 1) + 4 * T.n_pieces + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
+  // two input buffers, two message buffers (the bulk store of one batch drains while the next is built)
+  b.warp_bytes = 2 * b.in_cap + 2 * b.msg_cap + static_cast<uint32_t>(16 * ((G * 4 + 15) / 16));
+  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
   if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
     return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
   return HAMMING_OK;
@@ -576,19 +582,18 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   __shared__ unsigned long long cta_counts[2];
   __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Wp = T.Wp, ns = T.n_special;
-  // CTA tables: word descriptors {word of slice 0, word of slice 1, shifts, nb},
-  // head words, pieces, per-segment geometry
+  const uint32_t Wp = T.Wp, npc = T.n_pieces;
+  // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
+  // pieces {src | len | pos, word}, per-segment geometry
   uint4* wdesc = reinterpret_cast<uint4*>(smem);
-  uint32_t* spec = reinterpret_cast<uint32_t*>(smem + 16 * Wp);
-  uint32_t* pieces = spec + kPktMaxSpecial + 1;
-  uint32_t* sg = pieces + T.n_pieces;  // [off | n | k | moff] x kPktMaxSeg
+  uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * Wp);
+  uint32_t* sg = reinterpret_cast<uint32_t*>(pieces + T.n_pieces);  // [off | n | k | moff] x kPktMaxSeg
   for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
-    wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, 0u);
+    const bool head = nb > 32;  // head words are 0 after pass R and OR-ed together by pass H
+    wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, head ? 0u : 0xFFFFFFFFu);
   }
-  for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) spec[i] = T.special[i];
-  for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = T.piece[i];
+  for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = make_uint2(T.piece[i], T.piece_word[i]);
   if (threadIdx.x < g.t) {
     sg[threadIdx.x] = g.off[threadIdx.x];
     sg[kPktMaxSeg + threadIdx.x] = g.n[threadIdx.x];
@@ -596,8 +601,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     sg[3 * kPktMaxSeg + threadIdx.x] = g.moff[threadIdx.x];
   }
   uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
-  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap);
-  uint32_t* pst = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + bg.msg_cap);  // per-packet status
+  uint32_t* pst = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + 2 * bg.msg_cap);  // per-packet status
   uint64_t* bars = bars_all + warp * 2;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
@@ -634,43 +638,40 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     const uint64_t p0 = b * bg.G;
     const uint64_t left = a.n_packets - p0;
     const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
+    uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + buf * bg.msg_cap);
+    if (lane == 0) bulk_wait_read<1>();  // the bulk store issued two batches ago has read this mbuf
     for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
     mbar_wait(&bars[buf], (it >> 1) & 1u);
     __syncwarp();
-    {  // pass R: every word as one or two slices (head words are rewritten by pass H)
+    {  // pass R: every word as one or two slices (lane: word W of every packet of the batch)
       const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
-      uint32_t p = 0, W = lane;
-      if (W >= Wp) p = divmod_small(W, Wp, T.mag_wp, W);
-      const uint32_t total = np * Wp;
-      for (uint32_t u = lane; u < total; u += 32) {
-        const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, -}
-        const uint32_t* wp = w + 4 + p * wstride + d.x;  // (after the 16-byte pad)
-        const uint32_t a0 = wp[0], a1 = wp[1];
-        // slice 1 is the stream one bit further on (the parity position skipped)
-        mbuf[u] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
-        W += 32;
-        if (W >= Wp) {
-          W -= Wp;
-          ++p;
-          if (W >= Wp) p += divmod_small(W, Wp, T.mag_wp, W);  // only when Wp < 32
+      if (np == 1) {  // one packet per batch (long packets): no inner loop
+        for (uint32_t W = lane; W < Wp; W += 32) {
+          const uint4 d = wdesc[W];
+          const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
+          mbuf[W] = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+        }
+      } else
+      for (uint32_t W = lane; W < Wp; W += 32) {
+        const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
+        const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
+        uint32_t* mp = mbuf + W;
+        for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
+          const uint32_t a0 = wp[0], a1 = wp[1];
+          // slice 1 is the stream one bit further on (the parity position skipped)
+          *mp = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
         }
       }
     }
     __syncwarp();
-    if (ns > 0) {  // pass H: head words from their piece lists
-      for (uint32_t e = lane; e < np * ns; e += 32) {
-        uint32_t i;
-        const uint32_t p = divmod_small(e, ns, T.mag_ns, i);
-        const uint32_t sp = spec[i], pe = spec[i + 1] >> 16;
-        const uint32_t base = kPadBits + p * stride_bits;
-        uint32_t v = 0;
-        for (uint32_t c = sp >> 16; c < pe; ++c) {
-          const uint32_t pc = pieces[c];
-          const uint32_t s0 = base + (pc & 0xFFFFu), len = (pc >> 16) & 63u;
-          const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
-          v |= x << ((pc >> 24) & 31u);
-        }
-        mbuf[p * Wp + (sp & 0xFFFFu)] = v;
+    if (npc > 0) {  // pass H: head words, one piece per lane, OR-ed in
+      for (uint32_t e = lane; e < np * npc; e += 32) {
+        uint32_t c;
+        const uint32_t p = divmod_small(e, npc, T.mag_np, c);
+        const uint2 pc = pieces[c];
+        const uint32_t s0 = kPadBits + p * stride_bits + (pc.x & 0xFFFFu), len = (pc.x >> 16) & 63u;
+        const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
+        atomicOr(&mbuf[p * Wp + pc.y], x << ((pc.x >> 24) & 31u));
       }
     }
     __syncwarp();
@@ -709,8 +710,12 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
     const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + p0 * a.out_stride);
     if (a.out_stride == g.msg_bytes && (g.msg_bytes & 15u) == 0 && (ob & 15u) == 0) {
-      uint4* dst = reinterpret_cast<uint4*>(ob);
-      for (uint32_t i = lane; i < np * g.msg_bytes / 16; i += 32) dst[i] = reinterpret_cast<const uint4*>(mbuf)[i];
+      fence_proxy_async_smem();  // this lane's st.shared / atomics visible to the bulk copy
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g(reinterpret_cast<void*>(ob), mbuf, np * g.msg_bytes, pol);
+        bulk_commit();
+      }
     } else if ((g.msg_bytes & 3u) == 0 && (a.out_stride & 3u) == 0 && (ob & 3u) == 0) {
       for (uint32_t pk = 0; pk < np; ++pk) {
         uint32_t* dst = reinterpret_cast<uint32_t*>(ob + pk * a.out_stride);
@@ -726,6 +731,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       for (uint32_t i = lane; i < np; i += 32) a.status[p0 + i] = static_cast<uint8_t>(pst[i]);
     __syncwarp();
   }
+  if (lane == 0) bulk_wait<0>();  // the last bulk stores have completed before shared memory goes away
   if (a.counts != nullptr) {
     n_corr = __reduce_add_sync(0xffffffffu, n_corr);
     n_fail = __reduce_add_sync(0xffffffffu, n_fail);
