@@ -26,7 +26,10 @@
 
 constexpr int kPktMaxSeg = 16;
 constexpr int kPktMaxMsgBytes = 4096;
-constexpr int kPktWarps = 8;
+#ifndef HAM_PKT_WARPS
+#define HAM_PKT_WARPS 16
+#endif
+constexpr int kPktWarps = HAM_PKT_WARPS;
 
 struct PacketGeom {
   uint32_t msg_bytes, t, coded_bits, in_bytes;  // in_bytes = coded bytes rounded up to 16
@@ -276,6 +279,14 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
 // Every message word is written exactly once (R or H), so nothing is zeroed.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kPktMaxWords = kPktMaxMsgBytes / 4;
+#ifndef HAM_PKT_STAGES
+#define HAM_PKT_STAGES 2
+#endif
+#ifndef HAM_PKT_MSGBUF
+#define HAM_PKT_MSGBUF 1
+#endif
+constexpr uint32_t kPktStages = HAM_PKT_STAGES;   // input batches per warp (1 decoding + prefetch)
+constexpr int kPktMsgBufs = HAM_PKT_MSGBUF;       // message buffers per warp
 constexpr uint32_t kPktMaxSpecial = 80;   // <= 57 t / 32 + 2 t + 1 head words
 constexpr uint32_t kPktMaxPieces = 640;
 
@@ -359,18 +370,19 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   uint32_t L = 1;
   while (L < 32 && L * 8 < chunks) L *= 2;
 #ifndef HAM_PKT_BUDGET
-#define HAM_PKT_BUDGET (8 * 1024)
+#define HAM_PKT_BUDGET (6 * 1024)
 #endif
   const uint64_t budget = HAM_PKT_BUDGET;  // shared bytes per warp (tuned: tools/tune_shapes.py packets)
-  const uint64_t per = 2 * stride + 8ull * T.Wp + 4;
+  const uint64_t per = kPktStages * stride + kPktMsgBufs * 4ull * T.Wp + 4 + 4ull * g.t;
   uint64_t G = budget > 96 ? (budget - 96) / per : 1;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
   b.G = static_cast<uint32_t>(G);
   b.L = L;
   b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
   b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
-  // two input buffers, two message buffers (the bulk store of one batch drains while the next is built)
-  b.warp_bytes = 2 * b.in_cap + 2 * b.msg_cap + static_cast<uint32_t>(16 * ((G * 4 + 15) / 16));
+  // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
+  b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
+                 static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
   b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
   if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
     return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
@@ -459,6 +471,66 @@ __device__ __forceinline__ uint32_t group_syndrome_l(const uint32_t* w, uint32_t
     const uint32_t x = __funnelshift_r(w[(o >> 5) + j], w[(o >> 5) + j + 1], rb) & low_mask(n - 32 * j + 1);
     X ^= x;
     P ^= (__popc(x) & 1u) ? 32u * j : 0u;
+  }
+  if constexpr (L == 32) {
+    X = __reduce_xor_sync(0xffffffffu, X);
+    P = __reduce_xor_sync(0xffffffffu, P);
+  } else {
+#pragma unroll
+    for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
+      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
+      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
+    }
+  }
+  return P ^ xor_of_indices(X);
+}
+
+// The same syndrome over 64-position chunks (three shared loads per 64
+// positions): chunk J = positions 64 J .. 64 J + 63 = (lo, hi) with
+// Y_J = lo ^ hi, so X = XOR_J Y_J and
+//   XOR_j [32 j par(x_j)] = 64 XOR_J [J par(Y_J)] ^ 32 par(XOR_J hi_J).
+// Lane q takes J = q + L m, m = 4 blk + it (it < 4 unrolled), over the full
+// chunks (64 J + 63 <= n; position 0's garbage bit counts for nothing, as
+// above); with J = q | (L m): XOR over odd-parity J of J =
+// q par(X) ^ L (4 BB ^ par(A0) ^ 2 par(A1)).  The group's rank-0 lane adds
+// the tail (positions 64 Jf .. n, at most two masked 32-bit chunks).
+template <uint32_t L>
+__device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t off, uint32_t n, bool active,
+                                                     uint32_t q) {
+  const uint32_t o = off + kPadBits - 1;
+  const uint32_t rb = o & 31u;
+  const uint32_t full = active ? (n + 1) / 64 : 0;  // full 64-position chunks
+  const uint32_t* wq = w + (o >> 5) + 2 * q;
+  uint32_t X = 0, H = 0, A0 = 0, A1 = 0, BB = 0;
+  for (uint32_t blk = 0; 4 * L * blk < full; ++blk) {
+    const uint32_t* wb = wq + 8 * L * blk;
+    const int cnt = static_cast<int>(full - 4 * L * blk) - static_cast<int>(q);
+    uint32_t Xb = 0;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      if (static_cast<int>(L) * it < cnt) {
+        const uint32_t w0 = wb[2 * L * it], w1 = wb[2 * L * it + 1], w2 = wb[2 * L * it + 2];
+        const uint32_t hi = __funnelshift_r(w1, w2, rb);
+        const uint32_t y = __funnelshift_r(w0, w1, rb) ^ hi;
+        Xb ^= y;
+        H ^= hi;
+        if (it & 1) A0 ^= y;
+        if (it & 2) A1 ^= y;
+      }
+    }
+    X ^= Xb;
+    BB ^= (__popc(Xb) & 1u) ? blk : 0u;
+  }
+  uint32_t P = (64u * ((q * (__popc(X) & 1u)) ^ L * ((4u * BB) ^ (__popc(A0) & 1u) ^ ((__popc(A1) & 1u) << 1)))) ^
+               (32u * (__popc(H) & 1u));
+  if (active && q == 0) {  // the tail: positions 64 full .. n (fewer than 64)
+    const uint32_t j = 2 * full, b0 = (o >> 5) + j;
+    const uint32_t rest = n + 1 - 64 * full;  // positions left, 0 .. 63
+    const uint32_t lo = __funnelshift_r(w[b0], w[b0 + 1], rb) & __funnelshift_lc(0xFFFFFFFFu, 0u, rest);
+    const uint32_t hi = __funnelshift_r(w[b0 + 1], w[b0 + 2], rb) &
+                        __funnelshift_lc(0xFFFFFFFFu, 0u, rest > 32 ? rest - 32 : 0u);
+    X ^= lo ^ hi;
+    P ^= ((__popc(lo) & 1u) ? 32u * j : 0u) ^ ((__popc(hi) & 1u) ? 32u * (j + 1) : 0u);
   }
   if constexpr (L == 32) {
     X = __reduce_xor_sync(0xffffffffu, X);
@@ -580,7 +652,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
                           const __grid_constant__ PacketArgs a, const __grid_constant__ PacketTables T) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_counts[2];
-  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
+  __shared__ __align__(8) uint64_t bars_all[kPktWarps * kPktStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t Wp = T.Wp, npc = T.n_pieces;
   // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
@@ -601,8 +673,9 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     sg[3 * kPktMaxSeg + threadIdx.x] = g.moff[threadIdx.x];
   }
   uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
-  uint32_t* pst = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + 2 * bg.msg_cap);  // per-packet status
-  uint64_t* bars = bars_all + warp * 2;
+  uint32_t* pst = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + kPktMsgBufs * bg.msg_cap);  // statuses
+  uint32_t* sbuf = pst + bg.G;  // per-item syndromes of the batch
+  uint64_t* bars = bars_all + warp * kPktStages;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t n_batches = (a.n_packets + bg.G - 1) / bg.G;
@@ -619,10 +692,9 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     return static_cast<uint32_t>((left < bg.G ? left : bg.G) * a.in_stride);
   };
   if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (uint32_t s = 0; s < kPktStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    for (uint32_t s = 0; s < 2; ++s) {
+    for (uint32_t s = 0; s < kPktStages; ++s) {
       const uint64_t b = gw + s * nw;
       if (b < n_batches) {
         mbar_arrive_expect_tx(&bars[s], batch_bytes(b));
@@ -633,15 +705,15 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   __syncwarp();
   uint32_t it = 0;
   for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
-    const uint32_t buf = it & 1u;
+    const uint32_t buf = it % kPktStages;
     const uint32_t* w = reinterpret_cast<const uint32_t*>(wb + buf * bg.in_cap);
     const uint64_t p0 = b * bg.G;
     const uint64_t left = a.n_packets - p0;
     const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
-    uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * bg.in_cap + buf * bg.msg_cap);
-    if (lane == 0) bulk_wait_read<1>();  // the bulk store issued two batches ago has read this mbuf
+    uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + (it % kPktMsgBufs) * bg.msg_cap);
+    if (lane == 0) bulk_wait_read<kPktMsgBufs - 1>();  // the bulk store that last used this mbuf has read it
     for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
-    mbar_wait(&bars[buf], (it >> 1) & 1u);
+    mbar_wait(&bars[buf], (it / kPktStages) & 1u);
     __syncwarp();
     {  // pass R: every word as one or two slices (lane: word W of every packet of the batch)
       const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
@@ -675,7 +747,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       }
     }
     __syncwarp();
-    {  // pass S: syndromes; a correctable error flips its data bit in the message
+    {  // pass S: syndromes per (packet, segment) item, by groups of L lanes
       const uint32_t items = np * g.t;
       for (uint32_t base = 0; base < items; base += groups) {
         const bool active = base + gid < items;
@@ -683,24 +755,30 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         const uint32_t pk = divmod_small(active ? base + gid : 0, g.t, T.mag_t, seg);
         const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
         const uint32_t off = pk * stride_bits + sg[seg];
-        const uint32_t s = group_syndrome_l<L>(w, off, n, active, q);
-        if (active && q == 0) {
-          const bool corr = s != 0 && s <= n;
-          const bool fail = s > n;
-          if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
-          if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
-          n_corr += corr;
-          n_fail += fail;
-          if (corr && (s & (s - 1)) != 0) {  // a data position: message bit moff + s - floor(log2 s) - 2
-            const uint32_t fb = sg[3 * kPktMaxSeg + seg] + s - (31u - __clz(s)) - 2;
-            atomicXor(&mbuf[pk * Wp + (fb >> 5)], 1u << (fb & 31u));
-          }
-        }
+        const uint32_t s = group_syndrome64<L>(w, off, n, active, q);
+        if (active && q == 0) sbuf[base + gid] = s;
+      }
+    }
+    __syncwarp();
+    // per item: syndrome out, packet status, counts; a correctable error flips its data bit
+    for (uint32_t i = lane; i < np * g.t; i += 32) {
+      uint32_t seg;
+      const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
+      const uint32_t s = sbuf[i], n = sg[kPktMaxSeg + seg];
+      const bool corr = s != 0 && s <= n;
+      const bool fail = s > n;
+      if (a.syn != nullptr) a.syn[p0 * g.t + i] = static_cast<uint16_t>(s);
+      if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
+      n_corr += corr;
+      n_fail += fail;
+      if (corr && (s & (s - 1)) != 0) {  // a data position: message bit moff + s - floor(log2 s) - 2
+        const uint32_t fb = sg[3 * kPktMaxSeg + seg] + s - (31u - __clz(s)) - 2;
+        atomicXor(&mbuf[pk * Wp + (fb >> 5)], 1u << (fb & 31u));
       }
     }
     __syncwarp();
     if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
-      const uint64_t nx = b + 2 * nw;
+      const uint64_t nx = b + kPktStages * nw;
       if (nx < n_batches) {
         mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
         bulk_g2s(wb + buf * bg.in_cap + 16, a.in + nx * bg.G * a.in_stride, batch_bytes(nx), &bars[buf], pol);

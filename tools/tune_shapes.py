@@ -18,7 +18,7 @@ VARIANTS = {
 }
 
 
-PKT_BUDGETS = [4096, 6144, 8192, 12288, 16384, 24576]
+PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((5120, 2, 1, 16), (7168, 2, 1, 16), (6144, 2, 1, 12), (8192, 2, 1, 12), (4096, 2, 1, 32), (5120, 2, 1, 24), (6144, 2, 1, 20))]
 
 
 def name(m, v):
@@ -39,7 +39,9 @@ def build():
             defs = [f"HAM_W{m}={v[0]}", f"HAM_S{m}={v[1]}", f"HAM_IP{m}={'true' if v[2] else 'false'}"]
             jobs.append((os.path.join(OUT, name(m, v) + ".so"), defs))
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
-        jobs = [(os.path.join(OUT, f"pkt_{bud}.so"), [f"HAM_PKT_BUDGET={bud}"]) for bud in PKT_BUDGETS]
+        jobs = [(os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"),
+                 [f"HAM_PKT_BUDGET={b}", f"HAM_PKT_STAGES={st}", f"HAM_PKT_MSGBUF={mb}", f"HAM_PKT_WARPS={w}"])
+                for b, st, mb, w in PKT_VARIANTS]
     with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
         for path in ex.map(lambda j: b.build(force=True, out=j[0], defines=j[1]), jobs):
             print("built", path, flush=True)
@@ -47,9 +49,9 @@ def build():
 
 def run():
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
-        for bud in PKT_BUDGETS:
-            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{bud}.so"))
-            print("budget", bud, flush=True)
+        for b, st, mb, w in PKT_VARIANTS:
+            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"))
+            print("budget", b, "stages", st, "msgbufs", mb, "warps", w, flush=True)
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "1200",
                             "2000", "--t", "2", "6"], env=env)
         return
