@@ -628,6 +628,191 @@ struct DecodeLut4Op {
   }
 };
 
+
+// ------------------------------------------------ SECDED table decoders
+// Extended Hamming (2^m bits, bit 0 = overall parity P): the same decisions
+// as DecodeOp<m, true> -- P = 1: correct position s (s = 0: the parity bit);
+// P = 0, s != 0: double error detected, data left as received -- with the
+// syndrome from tables instead of POPCs.  The lane reads its 2^m words
+// through the swizzled tensor-map layout (swz_unit), like DecodeOp<m, true>.
+template <int IN_W>
+__device__ __forceinline__ void load_swizzled(const uint32_t* __restrict__ tile, uint32_t (&w)[IN_W]) {
+  constexpr int CPL = IN_W / 4;
+  const uint32_t l = threadIdx.x & 31u;
+#pragma unroll
+  for (int u = 0; u < CPL; ++u) {
+    const uint4 v = reinterpret_cast<const uint4*>(tile)[swz_unit<IN_W>(l * CPL + u)];
+    w[4 * u] = v.x;
+    w[4 * u + 1] = v.y;
+    w[4 * u + 2] = v.z;
+    w[4 * u + 3] = v.w;
+  }
+}
+
+// flags byte of a SECDED codeword from its syndrome and overall parity
+__device__ __forceinline__ uint32_t secded_flags(uint32_t s, uint32_t par) {
+  return s | (par << 6) | ((static_cast<uint32_t>(s != 0) & (par ^ 1u)) << 7);
+}
+
+// (8,4): a codeword is one byte; per-lane replicated 256-entry table (32 KB),
+// entry = final data nibble (bits 0..3) | flags << 8.
+struct DecodeSecded3Op {
+  static constexpr int NCOUNT = 2;
+  static constexpr int IN_W = 8, OUT_W = 4, IN_BITS = 8;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr bool SWZ = true;
+  static constexpr int SHARED = 256 * 32 * 4;
+  struct Args {
+    CUtensorMap tmap;
+  };
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += __popc(sw[i] & 0x40404040u);
+    return c;
+  }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&sw)[8]) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += __popc(sw[i] & 0x80808080u);
+    return c;
+  }
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    uint32_t* L = reinterpret_cast<uint32_t*>(sh);
+    for (int e = tid; e < 256 * 32; e += nth) {
+      uint32_t v = static_cast<uint32_t>(e >> 5);  // bit p = position p, bit 0 = P
+      const uint32_t s = syndrome_cw<3>(v, 0u);
+      const uint32_t par = static_cast<uint32_t>(__popc(v)) & 1u;
+      v ^= par << s;
+      const uint32_t d = ((v >> 3) & 1u) | ((v >> 4) & 0xEu);  // positions 3, 5, 6, 7
+      L[e] = d | (secded_flags(s, par) << 8);
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[8];
+    load_swizzled<8>(in, w);
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t off = (((w[c >> 2] >> (8 * (c & 3))) & 0xFFu) << 7) | lane4;  // (x * 32 + lane) * 4
+      const uint32_t e = *reinterpret_cast<const uint32_t*>(sh + off);
+      const int r = (4 * c) & 31;
+      o[c >> 3] |= (e & 0xFu) << r;
+      side[c >> 2] = insert_byte1(side[c >> 2], e, c & 3);
+    }
+    *reinterpret_cast<uint4*>(out) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+};
+
+// (16,11): positions 1..15 through the (15,11) table g_lut15 (corrected data |
+// s << 12), P = parity of the 16 bits (one POPC); a detected double error
+// takes the uncorrected data back by XOR-ing the data bit of position s
+// (per-lane table F[s], 2 KB, conflict-free).
+struct DecodeSecded4Op {
+  static constexpr int NCOUNT = 2;
+  static constexpr int IN_W = 16, OUT_W = 11, IN_BITS = 16;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr bool SWZ = true;
+  static constexpr int SHARED = 32768 * 2 + 16 * 32 * 4;
+  struct Args {
+    CUtensorMap tmap;
+  };
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return DecodeSecded3Op::count0(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&sw)[8]) { return DecodeSecded3Op::count1(sw); }
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    const uint4* src = reinterpret_cast<const uint4*>(g_lut15);
+    uint4* dst = reinterpret_cast<uint4*>(sh);
+    for (int i = tid; i < 32768 * 2 / 16; i += nth) dst[i] = src[i];
+    uint32_t* F = reinterpret_cast<uint32_t*>(sh + 32768 * 2);
+    for (int e = tid; e < 16 * 32; e += nth) {  // F[s][lane] = the data bit of position s (0 if parity)
+      const uint32_t v = (e >> 5) ? (1u << (e >> 5)) : 0u;
+      uint32_t raw = 0;
+#pragma unroll
+      for (int g = 1; g < 4; ++g) raw |= (v >> (g + 2)) & dmask(g);
+      F[e] = raw;
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[16];
+    load_swizzled<16>(in, w);
+    __syncwarp();
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[11];
+#pragma unroll
+    for (int i = 0; i < 11; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t cw = (w[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+      const uint32_t e = *reinterpret_cast<const uint16_t*>(sh + (cw & 0xFFFEu));  // positions 1..15, x 2
+      const uint32_t s = e >> 12, par = static_cast<uint32_t>(__popc(cw)) & 1u;
+      const uint32_t f = *reinterpret_cast<const uint32_t*>(sh + 65536 + (s << 7) + lane4);
+      const uint32_t d = (e ^ (par ? 0u : f)) & 0x7FFu;
+      const int b = 11 * c, q = b >> 5, r = b & 31;
+      o[q] |= d << r;
+      if (r > 21) o[q + 1] |= d >> (32 - r);
+      side[c >> 2] |= secded_flags(s, par) << (8 * (c & 3));
+    }
+#pragma unroll
+    for (int i = 0; i < 11; ++i) out[i] = o[i];
+  }
+};
+
+// (32,26): a codeword is one word; positions 1..15 and 17..31 through the
+// half-word table g_lut15raw (uncorrected RR | syndrome part << 11 | parity
+// << 15) as in DecodeLut5Op; P = both parities ^ bit 16 ^ bit 0 -- no POPC.
+struct DecodeSecded5Op {
+  static constexpr int NCOUNT = 2;
+  static constexpr int IN_W = 32, OUT_W = 26, IN_BITS = 32;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr bool SWZ = true;
+  static constexpr int SHARED = 32768 * 2 + 32 * 32 * 4;
+  struct Args {
+    CUtensorMap tmap;
+  };
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return DecodeSecded3Op::count0(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&sw)[8]) { return DecodeSecded3Op::count1(sw); }
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) { DecodeLut5Op::cta_init(sh, tid, nth); }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&,
+                                              const uint8_t* sh) {
+    uint32_t w[32];
+    load_swizzled<32>(in, w);
+    __syncwarp();
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[26];
+#pragma unroll
+    for (int i = 0; i < 26; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t x = w[c];
+      const uint32_t elo = *reinterpret_cast<const uint16_t*>(sh + (x & 0xFFFEu));          // positions 1..15
+      const uint32_t h = x >> 16;                                                            // 16, 17..31
+      const uint32_t ehi = *reinterpret_cast<const uint16_t*>(sh + (h & 0xFFFEu));
+      const uint32_t t = elo ^ ehi;
+      const uint32_t s = ((t >> 11) & 0xFu) | ((((ehi >> 15) ^ h) & 1u) << 4);
+      const uint32_t par = ((t >> 15) ^ h ^ x) & 1u;  // parities of both halves, bit 16, bit 0
+      const uint32_t f = *reinterpret_cast<const uint32_t*>(sh + 65536 + (s << 7) + lane4);
+      const uint32_t d = ((elo & 0x7FFu) | ((h << 10) & 0x3FFF800u)) ^ (par ? f : 0u);
+      put_bits(o, 26 * c, d, 26);
+      side[c >> 2] |= secded_flags(s, par) << (8 * (c & 3));
+    }
+#pragma unroll
+    for (int i = 0; i < 26; ++i) out[i] = o[i];
+  }
+};
+
 // SECDED: set bit 0 (position 0) to the parity of positions 1..n and emit the
 // whole 2^m-bit codeword at lane-stream bit b.
 template <int M, int NO>
@@ -1497,6 +1682,23 @@ uint64_t hamming_secded_coded_bytes(int m, uint64_t N) {
   return (N << m) / 8;
 }
 
+// SECDED launch shapes (warps x stages), tunable with -D (tools/tune_shapes.py secded)
+#ifndef HAM_SEC_W3
+#define HAM_SEC_W3 16
+#define HAM_SEC_S3 4
+#endif
+#ifndef HAM_SEC_W4
+#define HAM_SEC_W4 16
+#define HAM_SEC_S4 3
+#endif
+#ifndef HAM_SEC_W5
+#define HAM_SEC_W5 12
+#define HAM_SEC_S5 3
+#endif
+#ifndef HAM_SEC_W6
+#define HAM_SEC_W6 8
+#define HAM_SEC_S6 3
+#endif
 hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void* data_dev, uint8_t* flags_dev,
                                      unsigned long long* counts_dev, void* stream) {
   g_launches = 0;
@@ -1516,23 +1718,26 @@ hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint8_t* in = static_cast<const uint8_t*>(rx_dev);
   uint8_t* out = static_cast<uint8_t*>(data_dev);
+  if (m == 4 || m == 5) {  // the (15,11) / half-word tables
+    int dev = 0;
+    const cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    const hamming_status rc = ensure_lut15(dev);
+    if (rc != HAMMING_OK) return rc;
+  }
   if (N < kSmallPacketCw) {
     switch (m) {
-#define HAMMING_SECDED_SMALL(MM) \
-  case MM:                       \
-    return run_swizzled<DecodeOp<MM, true>, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
-      HAMMING_SECDED_SMALL(3)
-      HAMMING_SECDED_SMALL(4)
-      HAMMING_SECDED_SMALL(5)
-      HAMMING_SECDED_SMALL(6)
-#undef HAMMING_SECDED_SMALL
+      case 3: return run_swizzled<DecodeSecded3Op, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+      case 4: return run_swizzled<DecodeSecded4Op, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+      case 5: return run_swizzled<DecodeSecded5Op, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+      case 6: return run_swizzled<DecodeOp<6, true>, 4, 2>(in, out, flags_dev, N, ib, ob, counts_dev, st);
     }
   }
   switch (m) {
-    case 3: return run_swizzled<DecodeOp<3, true>, 16, 8>(in, out, flags_dev, N, ib, ob, counts_dev, st);
-    case 4: return run_swizzled<DecodeOp<4, true>, 16, 6>(in, out, flags_dev, N, ib, ob, counts_dev, st);
-    case 5: return run_swizzled<DecodeOp<5, true>, 12, 3>(in, out, flags_dev, N, ib, ob, counts_dev, st);
-    case 6: return run_swizzled<DecodeOp<6, true>, 8, 3>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 3: return run_swizzled<DecodeSecded3Op, HAM_SEC_W3, HAM_SEC_S3>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 4: return run_swizzled<DecodeSecded4Op, HAM_SEC_W4, HAM_SEC_S4>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 5: return run_swizzled<DecodeSecded5Op, HAM_SEC_W5, HAM_SEC_S5>(in, out, flags_dev, N, ib, ob, counts_dev, st);
+    case 6: return run_swizzled<DecodeOp<6, true>, HAM_SEC_W6, HAM_SEC_S6>(in, out, flags_dev, N, ib, ob, counts_dev, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_decode_secded: m must be in [3, 6]");
 }

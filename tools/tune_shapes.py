@@ -18,6 +18,12 @@ VARIANTS = {
 }
 
 
+SECDED_VARIANTS = {
+    3: [(16, 8), (8, 12), (16, 4), (24, 4)],
+    4: [(8, 8), (16, 3), (12, 4), (8, 12), (16, 4)],
+    5: [(12, 3), (8, 4), (16, 2), (8, 3)],
+    6: [(8, 3), (12, 2), (8, 2)],
+}
 PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((5120, 2, 1, 16), (7168, 2, 1, 16), (6144, 2, 1, 12), (8192, 2, 1, 12), (4096, 2, 1, 32), (5120, 2, 1, 24), (6144, 2, 1, 20))]
 
 
@@ -38,6 +44,9 @@ def build():
             # the other m keep their defaults
             defs = [f"HAM_W{m}={v[0]}", f"HAM_S{m}={v[1]}", f"HAM_IP{m}={'true' if v[2] else 'false'}"]
             jobs.append((os.path.join(OUT, name(m, v) + ".so"), defs))
+    if len(sys.argv) > 2 and sys.argv[2] == "secded":
+        jobs = [(os.path.join(OUT, f"sec_m{m}_w{w}_s{st}.so"), [f"HAM_SEC_W{m}={w}", f"HAM_SEC_S{m}={st}"])
+                for m, vs in SECDED_VARIANTS.items() for w, st in vs]
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
         jobs = [(os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"),
                  [f"HAM_PKT_BUDGET={b}", f"HAM_PKT_STAGES={st}", f"HAM_PKT_MSGBUF={mb}", f"HAM_PKT_WARPS={w}"])
@@ -48,6 +57,13 @@ def build():
 
 
 def run():
+    if len(sys.argv) > 2 and sys.argv[2] == "secded":
+        for m, vs in SECDED_VARIANTS.items():
+            for w, st in vs:
+                env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"sec_m{m}_w{w}_s{st}.so"))
+                subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--secded", "--m",
+                                str(m), "--tag", f"w{w}_s{st}"], env=env)
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
         for b, st, mb, w in PKT_VARIANTS:
             env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"))
