@@ -9,20 +9,13 @@
 // n up to 8013 bits on the paper's grid (M = 400..2000 B, t = 2..6).
 // The encoded packet is H = H_1 + ... + H_t, LSB-first (reading R4).
 //
-// GPU design: one warp per packet (grid-stride over packets), the packet
-// staged in shared memory with coalesced 128-bit loads.
-// Per segment:
-//   syndrome (the checksum vector): position p = 32 j + b, so
-//     s = XOR_j [32 j * parity(x_j)]  ^  S5( XOR_j x_j ),
-//   where x_j is the 32-position chunk j and S5(x) = XOR of the bit indices
-//   of x (five POPCs).  S5 is linear, so each lane XORs its chunks and pays
-//   one POPC per chunk for the parity; one warp XOR-reduction; S5 once.
-//   ED/EC: s = 0 clean; 1 <= s <= n flip bit s (one lane, in shared memory);
-//   s > n names a non-existent position: uncorrectable, bits left as received
-//   (reading R15; SPEC detect_and_correct).
-//   RR + merger: data index d of position p in run j (2^j < p < 2^(j+1)) is
-//   p - j - 2, so every 32-bit word of the message is 1..3 funnel-shifted
-//   slices of the packet stream; lanes build consecutive message words.
+// GPU design.  Encoder / synthetic channel (not the hot path): one warp per
+// packet, the packet staged in shared memory.  Decoder: packets_decode_kernel
+// (below) -- a warp decodes a batch of packets from shared memory in passes
+// driven by host-built per-word slice tables; its syndrome is the checksum
+// vector of P:L160 over 64-position chunks, s > n is the uncorrectable path
+// (reading R15; SPEC detect_and_correct).  m = 7, 8 perfect-code streams:
+// perfect_long_kernel (end of file).
 
 constexpr int kPktMaxSeg = 16;
 constexpr int kPktMaxMsgBytes = 4096;
@@ -91,14 +84,6 @@ __device__ __forceinline__ uint32_t xor_of_indices(uint32_t x) {
 // -- is still inside the buffer and every chunk is one funnel shift.
 constexpr uint32_t kPadBits = 128;
 
-// Data index -> run: the data bits of run j (positions 2^j+1 .. 2^(j+1)-1) are
-// d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2.  Closed form
-// j = floor(log2(d + floor(log2(d + 2)) + 2)) (checked exhaustively for
-// d < 200000, far past the largest segment).
-__device__ __forceinline__ uint32_t run_of(uint32_t d) {
-  const uint32_t j0 = 31u - __clz(d + 2);
-  return 31u - __clz(d + j0 + 2);
-}
 
 // Encoder side: codeword word cw (positions 32 cw .. 32 cw + 31) of segment
 // (k, moff) built from the message words `msg` -- data positions only (parity
@@ -303,7 +288,8 @@ struct PacketTables {
 };
 // src = bit of the packet stream (from its first bit) holding the slice's first data bit.
 
-// host: data index -> run j (data indices of run j: 2^j-j-1 .. 2^(j+1)-j-3)
+// host: data index -> run j: the data bits of run j (positions 2^j+1 .. 2^(j+1)-1)
+// are d in [2^j - j - 1, 2^(j+1) - j - 3]; position = d + j + 2
 uint32_t host_run_of(uint32_t d) {
   uint32_t j = 1;
   while (d >= (2u << j) - j - 2) ++j;
@@ -389,102 +375,6 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   return HAMMING_OK;
 }
 
-// Syndrome of item (off, n) by a group of L lanes (rank q); all 32 lanes call
-// it together (inactive groups pass active = false).  Interior chunks need no
-// mask; the group's rank-0 lane adds the first chunk (position 0 masked off)
-// and the last one (positions past n masked off).
-__device__ __forceinline__ uint32_t group_syndrome(const uint32_t* w, uint32_t off, uint32_t n, bool active,
-                                                   uint32_t q, uint32_t L) {
-  const uint32_t chunks = active ? (n + 32) / 32 : 0;
-  const uint32_t o = off + kPadBits - 1;
-  const uint32_t qb = o >> 5, rb = o & 31u;
-  uint32_t X = 0, P = 0;
-  for (uint32_t j = 1 + q; j + 1 < chunks; j += L) {
-    const uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb);
-    X ^= x;
-    P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
-  }
-  if (active && q == 0) {
-    uint32_t x0 = __funnelshift_r(w[qb], w[qb + 1], rb) & 0xFFFFFFFEu;
-    if (chunks == 1) x0 &= low_mask(n + 1);
-    X ^= x0;
-    if (chunks > 1) {
-      const uint32_t j = chunks - 1;
-      const uint32_t x = __funnelshift_r(w[qb + j], w[qb + j + 1], rb) & low_mask(n - 32 * j + 1);
-      X ^= x;
-      P ^= (static_cast<uint32_t>(__popc(x)) & 1u) * (32u * j);
-    }
-  }
-  if (L == 32) {  // one REDUX each for a whole-warp item
-    X = __reduce_xor_sync(0xffffffffu, X);
-    P = __reduce_xor_sync(0xffffffffu, P);
-  } else {
-    for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
-      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
-      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
-    }
-  }
-  return P ^ xor_of_indices(X);
-}
-
-// The same syndrome with L a compile-time group size and no per-chunk POPC.
-// Lane q takes chunks j = q + L m, m = 8 blk + it (it < 8, unrolled), over
-// j = 0 .. C-2 unmasked (position 0 sits in chunk 0, which contributes 0 to
-// both halves of s whatever its bits), and the group's rank-0 lane adds the
-// last chunk masked to positions <= n.  The high part XOR_j [32 j par(x_j)]
-// is rebuilt at the end from parities of a few accumulators: with q < L a
-// power of two, j = q | (L m), so XOR over odd-parity chunks of j is
-// q*par(X) ^ L*(8*BB ^ par(A0) ^ 2 par(A1) ^ 4 par(A2)), where A_b is the XOR
-// of the chunks whose `it` has bit b and BB the XOR of the block indices with
-// an odd block parity.
-template <uint32_t L>
-__device__ __forceinline__ uint32_t group_syndrome_l(const uint32_t* w, uint32_t off, uint32_t n, bool active,
-                                                     uint32_t q) {
-  const uint32_t C = active ? (n + 32) / 32 : 0;
-  const uint32_t o = off + kPadBits - 1;
-  const uint32_t* wq = w + (o >> 5) + q;
-  const uint32_t rb = o & 31u;
-  uint32_t X = 0, A0 = 0, A1 = 0, A2 = 0, BB = 0;
-  const uint32_t interior = C > 0 ? C - 1 : 0;  // chunks 0 .. C-2
-  for (uint32_t blk = 0; 8 * L * blk < interior; ++blk) {
-    const uint32_t* wb = wq + 8 * L * blk;
-    // chunks of this lane in the block: j = q + 8 L blk + L it < interior
-    const int cnt = static_cast<int>(interior - 8 * L * blk) - static_cast<int>(q);
-    uint32_t Xb = 0;
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      if (static_cast<int>(L) * it < cnt) {
-        const uint32_t x = __funnelshift_r(wb[L * it], wb[L * it + 1], rb);
-        Xb ^= x;
-        if (it & 1) A0 ^= x;
-        if (it & 2) A1 ^= x;
-        if (it & 4) A2 ^= x;
-      }
-    }
-    X ^= Xb;
-    BB ^= (__popc(Xb) & 1u) ? blk : 0u;
-  }
-  uint32_t P = 32u * ((q * (__popc(X) & 1u)) ^
-                      L * ((8u * BB) ^ (__popc(A0) & 1u) ^ ((__popc(A1) & 1u) << 1) ^ ((__popc(A2) & 1u) << 2)));
-  if (active && q == 0) {  // the last chunk, positions past n masked off
-    const uint32_t j = C - 1;
-    const uint32_t x = __funnelshift_r(w[(o >> 5) + j], w[(o >> 5) + j + 1], rb) & low_mask(n - 32 * j + 1);
-    X ^= x;
-    P ^= (__popc(x) & 1u) ? 32u * j : 0u;
-  }
-  if constexpr (L == 32) {
-    X = __reduce_xor_sync(0xffffffffu, X);
-    P = __reduce_xor_sync(0xffffffffu, P);
-  } else {
-#pragma unroll
-    for (uint32_t sh = L >> 1; sh > 0; sh >>= 1) {
-      X ^= __shfl_xor_sync(0xffffffffu, X, sh);
-      P ^= __shfl_xor_sync(0xffffffffu, P, sh);
-    }
-  }
-  return P ^ xor_of_indices(X);
-}
-
 // The same syndrome over 64-position chunks (three shared loads per 64
 // positions): chunk J = positions 64 J .. 64 J + 63 = (lo, hi) with
 // Y_J = lo ^ hi, so X = XOR_J Y_J and
@@ -543,95 +433,6 @@ __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t
     }
   }
   return P ^ xor_of_indices(X);
-}
-
-// The first 57 data bits of an item (positions 3..63 -- runs 1..5, where
-// the run boundaries are dense) by the fixed compaction of the (63,57) code:
-// v = positions 0..63, groups g = 1..4 from the low word, positions 33..63
-// from the high word.  Bits past k are garbage and are masked by the caller.
-__device__ __forceinline__ uint64_t rr_head57(const uint32_t* w, uint32_t off) {
-  const uint32_t o = off + kPadBits - 1;  // buffer bit of position 0
-  const uint32_t q = o >> 5, r = o & 31u;
-  const uint32_t lo = __funnelshift_r(w[q], w[q + 1], r);
-  const uint32_t hi = __funnelshift_r(w[q + 1], w[q + 2], r);
-  uint32_t d = 0;
-#pragma unroll
-  for (int g = 1; g < 5; ++g) d |= (lo >> (g + 2)) & dmask(g);
-  return static_cast<uint64_t>(d) | (static_cast<uint64_t>(hi >> 1) << 26);
-}
-
-// One message word of an item, general form (edge words, words holding
-// d < 57): bits of the word outside [moff, moff + k) are 0.
-__device__ __forceinline__ uint32_t item_word_general(const uint32_t* w, uint64_t head, uint32_t off, uint32_t k,
-                                                      uint32_t moff, uint32_t mw) {
-  const uint32_t d0 = max(32u * mw, moff) - moff;
-  const uint32_t d1 = min(32u * mw + 32u, moff + k) - moff;
-  const uint32_t sh = moff + d0 - 32u * mw;  // bit of the word that receives d0
-  uint32_t v = 0;
-  if (d0 < 57u) {
-    const uint32_t e = min(d1, 57u);
-    v = (static_cast<uint32_t>(head >> d0) & low_mask(e - d0)) << sh;
-  }
-  if (d1 > 57u) {
-    const uint32_t dd = max(d0, 57u);
-    const uint32_t j = run_of(dd);
-    const uint32_t nb = min(32u, (2u << j) - j - 2 - dd);  // bits before the next run starts
-    const uint32_t src = off + kPadBits + dd + j + 1;
-    const uint32_t x0 = sm_bits32(w, src), x1 = sm_bits32(w, src + 1);
-    const uint32_t part = ((x0 & low_mask(nb)) | (x1 & ~low_mask(nb))) & low_mask(d1 - dd);
-    v |= part << (sh + dd - d0);
-  }
-  return v;
-}
-
-// Redundancy removal + merger for one item by its group: lane q builds message
-// words mw0 + q, mw0 + q + L, ...  Data index d sits in run j at buffer bit
-// off + kPadBits + d + j + 1.  d < 57 comes from rr_head57; from d = 57 on
-// every run is >= 63 bits long, so a 32-bit window holds at most one run
-// boundary: an interior word is two funnel-shifted slices one bit apart,
-// merged at the boundary (branch free, the run tracked incrementally per
-// lane).  Interior words are stored; the item's edge words (shared with
-// neighbours) and the words holding d < 57 take the general path and are
-// OR-ed atomically.  fb = message bit to flip (the corrected data bit) or ~0.
-__device__ __forceinline__ void group_rr(const uint32_t* w, uint32_t* mbuf, uint32_t off, uint32_t k,
-                                         uint32_t moff, uint32_t fb, uint32_t q, uint32_t L) {
-  const uint32_t mw0 = moff / 32, mw1 = (moff + k + 31) / 32;
-  // interior words: wholly inside the item and wholly at d >= 57
-  const uint32_t ia = max((moff + 57 + 31) / 32, (moff + 31) / 32), ib = (moff + k) / 32;
-  uint64_t head = 0;
-  if (q < 3) head = rr_head57(w, off);  // the words holding d < 57 are the first (at most) three
-  // general words: the head [mw0, min(ia, mw1)) and the tail [max(ib, ia), mw1) -- a few each
-  const bool has_interior = ia < ib;
-  const uint32_t he = has_interior ? ia : mw1, ts = has_interior ? ib : mw1;
-  for (uint32_t i = q; i < (he - mw0) + (mw1 - ts); i += L) {
-    const uint32_t mw = (i < he - mw0) ? mw0 + i : ts + (i - (he - mw0));
-    uint32_t v = item_word_general(w, head, off, k, moff, mw);
-    if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
-    atomicOr(&mbuf[mw], v);
-  }
-  // interior words, lane q: ia + q', ia + q' + L, ... with q' the lane's slot in that sequence
-  uint32_t mw = ia + ((q + L - (ia - mw0) % L) % L);
-  if (has_interior && mw < ib) {
-    uint32_t dd = 32u * mw - moff;
-    uint32_t j = run_of(dd);
-    uint32_t nxt = (2u << j) - j - 2;   // first data index of run j + 1
-    const uint32_t base = off + kPadBits + 1;
-    for (; mw < ib; mw += L, dd += 32u * L) {
-      while (dd >= nxt) {
-        ++j;
-        nxt = (2u << j) - j - 2;
-      }
-      const uint32_t src = base + dd + j;
-      const uint32_t qw = src >> 5, r = src & 31u;
-      const uint32_t a0 = w[qw], a1 = w[qw + 1];
-      const uint32_t x0 = __funnelshift_r(a0, a1, r);                          // run j
-      const uint32_t x1 = (r == 31u) ? a1 : __funnelshift_r(a0, a1, r + 1);   // run j + 1: one bit later
-      const uint32_t lm = low_mask(min(32u, nxt - dd));
-      uint32_t v = (x0 & lm) | (x1 & ~lm);
-      if ((fb >> 5) == mw) v ^= 1u << (fb & 31u);
-      mbuf[mw] = v;
-    }
-  }
 }
 
 // q = u / d, r = u % d from mag = floor(2^32 / d) (2^32 - 1 for d = 1): the
@@ -873,12 +674,6 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   return HAMMING_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Longer perfect codes, m = 7, 8 ((127,120), (255,247); SURVEY.md 8(f) f4):
-// the same item engine over a stream of codewords -- a batch is 128
-// codewords (16n input bytes, 16k output bytes, both 16-byte aligned), items
-// are codewords (off = c n, moff = c k), one lane per codeword.
-// ---------------------------------------------------------------------------
 struct LongArgs {
   const uint8_t* in;
   uint8_t* out;
@@ -888,25 +683,150 @@ struct LongArgs {
   uint32_t n, k, store_count;
 };
 
-constexpr uint32_t kLongBatch = 128;
+// ---------------------------------------------------------------------------
+// Longer perfect codes, m = 7, 8 ((127,120), (255,247); SURVEY.md 8(f) f4):
+// one lane per codeword, 2^m codewords per batch.  With n = 2^m - 1 a batch
+// of 2^m codewords is exactly n UNITS of 2^m bits (UW = 2^m / 32 words, 16-
+// or 32-byte aligned), and codeword c's window -- positions 0..2^m-1, i.e.
+// stream bits [c n - 1, c n - 1 + 2^m) -- starts in unit c-1 at bit
+// 2^m - 1 - c.  With c = lane + 32 i that is word UW-1-i (the same for the
+// whole warp: i is unrolled) at bit 31 - lane, so a lane loads its own unit
+// c with vector loads and takes the tail words of unit c-1 from lane-1 by
+// shuffle (lane 0: from lane 31's previous unit): no bank conflicts, one
+// funnel shift per window word.  Syndrome: position p = 32 j + b, so
+// s = S5(XOR_j v_j) ^ 32 XOR_j [j par(v_j)] (m + 2 POPCs); flip; redundancy
+// removal = the (31,26) compaction of v_0 then v_1 >> 1, v_2 >> 1, v_3
+// (m = 8: v_4 >> 1, v_5..v_7); the k data bits are funnel-shifted to their
+// bit offset k*lane in the 32-codeword output block (k words, aligned), the
+// word shared with the next lane passed up by one shuffle, and staged in
+// shared memory for one TMA bulk store per batch.
+// ---------------------------------------------------------------------------
+template <int M>
+struct LongGeo {
+  static constexpr int UW = (1 << M) / 32;          // words per unit (= per codeword window)
+  static constexpr int n = (1 << M) - 1, k = n - M;
+  static constexpr int KW = (k + 31) / 32;           // data words per codeword
+  static constexpr int B = 1 << M;                   // codewords per batch
+  static constexpr int IN_BYTES = n * UW * 4;        // = B n / 8
+  static constexpr int OUT_BYTES = B * k / 8;
+};
 
-__global__ void __launch_bounds__(kPktWarps * 32)
-    long_decode_kernel(const __grid_constant__ LongArgs a) {
+template <int M>
+__device__ __forceinline__ uint32_t long_batch(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                               uint8_t* __restrict__ syn, uint32_t nvalid, uint32_t lane) {
+  using G = LongGeo<M>;
+  constexpr int UW = G::UW, k = G::k, KW = G::KW;
+  uint32_t cnt = 0;
+  uint32_t Uprev[UW];
+#pragma unroll
+  for (int j = 0; j < UW; ++j) Uprev[j] = 0;  // unit -1: only position 0 of codeword 0 (ignored)
+#pragma unroll
+  for (int i = 0; i < G::B / 32; ++i) {
+    const uint32_t c = lane + 32u * i;
+    uint32_t P[2 * UW];  // units c-1 and c
+    const uint4* up = reinterpret_cast<const uint4*>(in + c * UW);
+#pragma unroll
+    for (int q = 0; q < UW / 4; ++q) {
+      const uint4 x = up[q];
+      P[UW + 4 * q] = x.x;
+      P[UW + 4 * q + 1] = x.y;
+      P[UW + 4 * q + 2] = x.z;
+      P[UW + 4 * q + 3] = x.w;
+    }
+    const int w0 = UW - 1 - i;  // first window word (a constant: i is unrolled)
+#pragma unroll
+    for (int j = 0; j < UW; ++j) {
+      if (j >= w0) {
+        const uint32_t send = (lane == 31) ? Uprev[j] : P[UW + j];
+        P[j] = __shfl_sync(0xffffffffu, send, (lane + 31) & 31);
+      } else {
+        P[j] = 0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < UW; ++j) Uprev[j] = P[UW + j];
+    const uint32_t r = 31u - lane;
+    uint32_t v[UW];
+#pragma unroll
+    for (int j = 0; j < UW; ++j) v[j] = __funnelshift_r(P[w0 + j], P[w0 + j + 1], r);
+    // syndrome (a2): low five bits from the XOR of the window words, high bits from their parities
+    uint32_t X = 0;
+#pragma unroll
+    for (int j = 0; j < UW; ++j) X ^= v[j];
+    uint32_t s = xor_of_indices(X);
+#pragma unroll
+    for (int b = 0; (1 << b) < UW; ++b) {
+      uint32_t y = 0;
+#pragma unroll
+      for (int j = 0; j < UW; ++j)
+        if ((j >> b) & 1) y ^= v[j];
+      s |= (static_cast<uint32_t>(__popc(y)) & 1u) << (5 + b);
+    }
+    // a3: flip position s (s = 0: the dummy position 0)
+    const uint32_t fbit = 1u << (s & 31u);
+#pragma unroll
+    for (int j = 0; j < UW; ++j) v[j] ^= ((s >> 5) == static_cast<uint32_t>(j)) ? fbit : 0u;
+    // a4: redundancy removal into D (k bits)
+    uint32_t D[KW];
+#pragma unroll
+    for (int j = 0; j < KW; ++j) D[j] = 0;
+    uint32_t d0 = 0;
+#pragma unroll
+    for (int g = 1; g < 5; ++g) d0 |= (v[0] >> (g + 2)) & dmask(g);
+    put_bits(D, 0, d0, 26);
+    put_bits(D, 26, v[1] >> 1, 31);
+    put_bits(D, 57, v[2] >> 1, 31);
+    put_bits(D, 88, v[3], 32);
+    if constexpr (M == 8) {
+      put_bits(D, 120, v[4] >> 1, 31);
+      put_bits(D, 151, v[5], 32);
+      put_bits(D, 183, v[6], 32);
+      put_bits(D, 215, v[7], 32);
+    }
+    // a5: place the k bits at bit k*lane of this iteration's k-word output block
+    const uint32_t b0 = static_cast<uint32_t>(k) * lane, sh = b0 & 31u, q0 = b0 >> 5;
+    const uint32_t nw = ((b0 + k - 1) >> 5) - q0 + 1;
+    const bool end_partial = ((b0 + k) & 31u) != 0;
+    uint32_t O[KW + 1];
+    O[0] = D[0] << sh;
+#pragma unroll
+    for (int j = 1; j < KW; ++j) O[j] = __funnelshift_l(D[j - 1], D[j], sh);
+    O[KW] = __funnelshift_l(D[KW - 1], 0u, sh);
+    const uint32_t tail = (nw - 1 == static_cast<uint32_t>(KW)) ? O[KW] : O[KW - 1];
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, tail, 1);
+    if (sh != 0) O[0] |= prev;  // the word shared with lane - 1 (never lane 0: blocks are word-aligned)
+    uint32_t* ob = out + i * k + q0;
+#pragma unroll
+    for (int j = 0; j <= KW; ++j)
+      if (static_cast<uint32_t>(j) < nw && !(static_cast<uint32_t>(j) + 1 == nw && end_partial)) ob[j] = O[j];
+    if (c < nvalid) {
+      if (syn != nullptr) syn[c] = static_cast<uint8_t>(s);
+      cnt += (s != 0);
+    }
+  }
+  return cnt;
+}
+
+template <int M, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    perfect_long_kernel(const __grid_constant__ LongArgs a) {
+  using G = LongGeo<M>;
+  constexpr uint32_t IN_B = G::IN_BYTES, OUT_B = G::OUT_BYTES;
+  constexpr uint32_t WARP_BYTES = 2 * IN_B + OUT_B;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_count;
-  __shared__ __align__(8) uint64_t bars_all[kPktWarps * 2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t in_b = 16 * a.n, out_b = 16 * a.k;
-  const uint32_t in_cap = 16 + in_b + 16, msg_cap = out_b + 16;
-  uint8_t* wb = smem + warp * (2 * in_cap + msg_cap);
-  uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + 2 * in_cap);
+  __shared__ __align__(8) uint64_t bars_all[WARPS * 2];
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint8_t* wb = smem + warp * WARP_BYTES;
+  uint32_t* obuf = reinterpret_cast<uint32_t*>(wb + 2 * IN_B);
   uint64_t* bars = bars_all + warp * 2;
   if (threadIdx.x == 0) cta_count = 0;
   __syncthreads();
-  const uint64_t n_full = a.N / kLongBatch;
-  const uint64_t n_batches = (a.N + kLongBatch - 1) / kLongBatch;
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  const uint64_t n_full = a.N / G::B;
+  const uint64_t n_batches = (a.N + G::B - 1) / G::B;
+  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
   uint32_t cnt = 0;
   if (lane == 0) {
@@ -916,8 +836,8 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     for (uint32_t s = 0; s < 2; ++s) {
       const uint64_t b = gw + s * nw;
       if (b < n_full) {
-        mbar_arrive_expect_tx(&bars[s], in_b);
-        bulk_g2s(wb + s * in_cap + 16, a.in + b * in_b, in_b, &bars[s], pol);
+        mbar_arrive_expect_tx(&bars[s], IN_B);
+        bulk_g2s(wb + s * IN_B, a.in + b * IN_B, IN_B, &bars[s], pol);
       }
     }
   }
@@ -925,48 +845,43 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   uint32_t it = 0;
   for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
     const uint32_t buf = it & 1u;
-    uint8_t* wbytes = wb + buf * in_cap;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(wbytes);
+    uint8_t* ib = wb + buf * IN_B;
     const bool full = b < n_full;
-    const uint32_t nb = full ? kLongBatch : static_cast<uint32_t>(a.N - b * kLongBatch);
-    for (uint32_t i = lane; i < (out_b + 3) / 4; i += 32) mbuf[i] = 0;
+    const uint32_t nvalid = full ? G::B : static_cast<uint32_t>(a.N - b * G::B);
+    if (lane == 0) bulk_wait_read<0>();  // the previous batch's bulk store has read obuf
     if (full) {
       mbar_wait(&bars[buf], (it >> 1) & 1u);
-    } else {  // the ragged last batch: bounded loads (TMA needs whole 16-byte units)
-      const uint64_t ib0 = b * in_b, nbytes = a.in_total - ib0;
-      for (uint32_t i = lane; i < in_b; i += 32) wbytes[16 + i] = i < nbytes ? a.in[ib0 + i] : 0;
+    } else {  // the ragged last batch: bounded, zero-padded loads (TMA moves whole 16-byte units)
+      const uint64_t ib0 = b * IN_B, nbytes = a.in_total - ib0;
+      for (uint32_t i = lane; i < IN_B; i += 32) ib[i] = i < nbytes ? a.in[ib0 + i] : 0;
     }
     __syncwarp();
-    for (uint32_t c = lane; c < kLongBatch; c += 32) {  // all lanes take part in every round
-      const bool active = c < nb;
-      const uint32_t off = c * a.n, moff = c * a.k;
-      const uint32_t s = group_syndrome(w, off, a.n, active, 0, 1);
-      if (!active) continue;
-      uint32_t fb = 0xFFFFFFFFu;
-      if (s != 0 && (s & (s - 1)) != 0) fb = moff + s - (31u - __clz(s)) - 2;
-      group_rr(w, mbuf, off, a.k, moff, fb, 0, 1);
-      if (a.syn != nullptr) a.syn[b * kLongBatch + c] = static_cast<uint8_t>(s);
-      cnt += (s != 0);
-    }
+    cnt += long_batch<M>(reinterpret_cast<const uint32_t*>(ib), obuf,
+                         a.syn != nullptr ? a.syn + b * G::B : nullptr, nvalid, lane);
+    fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0 && full) {  // buffer consumed: prefetch the batch two steps ahead
-      const uint64_t nx = b + 2 * nw;
+    if (lane == 0 && full) {
+      bulk_s2g(a.out + b * OUT_B, obuf, OUT_B, pol);
+      bulk_commit();
+      const uint64_t nx = b + 2 * nw;  // the input buffer is consumed: prefetch two batches ahead
       if (nx < n_full) {
-        mbar_arrive_expect_tx(&bars[buf], in_b);
-        bulk_g2s(wbytes + 16, a.in + nx * in_b, in_b, &bars[buf], pol);
+        mbar_arrive_expect_tx(&bars[buf], IN_B);
+        bulk_g2s(ib, a.in + nx * IN_B, IN_B, &bars[buf], pol);
       }
     }
-    uint8_t* dst = a.out + b * out_b;
-    if (full) {
-      for (uint32_t i = lane; i < out_b / 16; i += 32)
-        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(mbuf)[i];
-    } else {
-      const uint64_t nbytes = a.out_total - b * out_b;
-      const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
-      for (uint32_t i = lane; i < nbytes; i += 32) dst[i] = mb[i];
+    if (!full) {  // bounded byte stores of the ragged batch
+      const uint64_t ob0 = b * OUT_B, nbytes = a.out_total - ob0;
+      const uint8_t* mb = reinterpret_cast<const uint8_t*>(obuf);
+      const uint32_t last_bits = static_cast<uint32_t>((a.N * G::k) & 7u);  // valid bits of the last byte
+      for (uint32_t i = lane; i < nbytes && i < OUT_B; i += 32) {
+        uint8_t x = mb[i];
+        if (i + 1 == nbytes && last_bits != 0) x &= static_cast<uint8_t>((1u << last_bits) - 1u);  // pad bits 0
+        a.out[ob0 + i] = x;
+      }
     }
     __syncwarp();
   }
+  if (lane == 0) bulk_wait<0>();
   if (a.counter != nullptr) {
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0 && cnt) atomicAdd(&cta_count, static_cast<unsigned long long>(cnt));
@@ -976,6 +891,40 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       else if (cta_count) atomicAdd(a.counter, cta_count);
     }
   }
+}
+
+template <int M, int WARPS>
+hamming_status launch_perfect_long(const LongArgs& a0, cudaStream_t st, bool accumulate) {
+  using G = LongGeo<M>;
+  LongArgs a = a0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  auto kfn = perfect_long_kernel<M, WARPS>;
+  const size_t smem = static_cast<size_t>(WARPS) * (2 * G::IN_BYTES + G::OUT_BYTES);
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(long decode)");
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, WARPS * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy(long decode)");
+  const uint64_t batches = (a.N + G::B - 1) / G::B;
+  const uint64_t want = (batches + WARPS - 1) / WARPS;
+  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+  a.store_count = (a.counter != nullptr && !accumulate && grid == 1) ? 1u : 0u;
+  if (a.counter != nullptr && !accumulate && !a.store_count) {
+    e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+  }
+  if (grid > 0) {
+    kfn<<<grid, WARPS * 32, smem, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "long decode launch");
+  }
+  g_launches = grid > 0 ? 1 : 0;
+  g_grid = grid;
+  return HAMMING_OK;
 }
 
 hamming_status launch_long_decode(int m, const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
@@ -990,34 +939,19 @@ hamming_status launch_long_decode(int m, const uint8_t* in, uint64_t N, uint8_t*
   a.N = N;
   a.in_total = (static_cast<uint64_t>(a.n) * N + 7) / 8;
   a.out_total = (static_cast<uint64_t>(a.k) * N + 7) / 8;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const size_t smem = static_cast<size_t>(kPktWarps) * (2 * (16 + 16 * a.n + 16) + 16 * a.k + 16);
-  e = cudaFuncSetAttribute(long_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(long decode)");
-  e = cudaFuncSetAttribute(long_decode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, long_decode_kernel, kPktWarps * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "occupancy(long decode)");
-  const uint64_t batches = (N + kLongBatch - 1) / kLongBatch;
-  const uint64_t want = (batches + kPktWarps - 1) / kPktWarps;
-  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
-  a.store_count = (counter != nullptr && !accumulate && grid == 1) ? 1u : 0u;
-  if (counter != nullptr && !accumulate && !a.store_count) {
-    e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+#ifndef HAM_LONG_W7
+#define HAM_LONG_W7 16
+#endif
+#ifndef HAM_LONG_W8
+#define HAM_LONG_W8 8
+#endif
+  if (N == 0 && counter != nullptr && !accumulate) {
+    const cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(corrected)");
+    g_launches = 0;
+    g_grid = 0;
+    return HAMMING_OK;
   }
-  if (grid > 0) {
-    long_decode_kernel<<<grid, kPktWarps * 32, smem, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "long decode launch");
-  } else if (counter != nullptr && !accumulate) {
-    e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
-  }
-  g_launches = grid > 0 ? 1 : 0;
-  g_grid = grid;
-  return HAMMING_OK;
+  if (m == 7) return launch_perfect_long<7, HAM_LONG_W7>(a, st, accumulate);
+  return launch_perfect_long<8, HAM_LONG_W8>(a, st, accumulate);
 }

@@ -186,7 +186,7 @@ def _noisy_codewords(oracle, m, N, seed, p_flip=0.4):
 
 
 @pytest.mark.parametrize("m", [7, 8])
-@pytest.mark.parametrize("N", [1, 31, 127, 128, 129, 1000, 4097])
+@pytest.mark.parametrize("N", [1, 31, 127, 128, 129, 255, 256, 257, 1000, 4097, 256 * 41, 300_001])
 def test_long_perfect_codes_match_oracle(oracle, m, N):
     """(127,120) and (255,247) through the long-codeword engine."""
     rx = _noisy_codewords(oracle, m, N, 1000 * m + N)

@@ -54,11 +54,12 @@ def test_generator_and_encoder_match_oracle(oracle, m):
         assert np.array_equal(enc.cpu().numpy()[: want.size], oracle.encode_secded(m, sent, N))
 
 
-def test_secded_large_counts(oracle):
-    """A 1 GiB (64,57) SECDED stream: corrected + detected counts equal the
-    channel's single / double events (closed form), flags agree with counts."""
-    m = 6
-    N = (1 << 30) * 8 // 64
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+def test_secded_large_counts(oracle, m):
+    """A 1 GiB SECDED stream (the multi-CTA table / POPC decoders): corrected +
+    detected counts equal the channel's single / double events (closed form),
+    flags agree with counts, a window matches the oracle."""
+    N = (1 << 30) * 8 // (1 << m)
     rx = ham.channel_generate_secded(m, 99, 0, N, p=0.2, q2=0.3)
     res = ham.decode_secded(m, rx, N)
     torch.cuda.synchronize()
@@ -70,6 +71,6 @@ def test_secded_large_counts(oracle):
     c0, w = (N // 2) // 8 * 8, 1 << 14
     rxw, _, _ = oracle.generate_secded(m, 99, c0, w, p=0.2, q2=0.3)
     wd, wf, _, _ = oracle.decode_secded(m, rxw, w)
-    k = 57
+    k = 2 ** m - 1 - m
     assert np.array_equal(res.data[c0 * k // 8: c0 * k // 8 + wd.size - 1].cpu().numpy(), wd[:-1])
     assert np.array_equal(f[c0: c0 + w].cpu().numpy(), wf)
