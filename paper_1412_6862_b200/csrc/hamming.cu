@@ -872,6 +872,73 @@ struct EncodeOp {
   }
 };
 
+// Table encoders (m = 3, 4; perfect and SECDED): the codeword is linear in
+// the data, so it is the XOR of one table entry per data chunk, each entry
+// the whole codeword (in stream form) of that chunk alone.  m = 3: a data
+// byte is two codewords, one 256-entry lookup per pair; m = 4: two lookups
+// (data bits 0..5, 6..10) per codeword.  Per-lane replicated tables (entry e
+// for lane l at word e * 32 + l: conflict free), built at CTA start from
+// encode_cw itself.  No POPC: the POPC encoder is XU-bound at m = 3, 4.
+template <int M, bool EXT = false>
+struct EncodeLutOp {
+  static_assert(M == 3 || M == 4, "table encoders: m = 3, 4");
+  static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
+  static constexpr int k = Geo<M>::k;
+  static constexpr int IN_W = k, OUT_W = CW_BITS, IN_BITS = k;
+  static constexpr bool HAS_SIDE = false;
+  static constexpr int NCOUNT = 1;
+  static constexpr int ENTRIES = (M == 3) ? 256 : 64 + 32;
+  static constexpr int SHARED = ENTRIES * 32 * 4;
+  struct Args {};
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&)[8]) { return 0; }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
+
+  // one codeword of data d, in stream form (perfect: positions 1..n; SECDED: bit 0 = P)
+  __device__ __forceinline__ static uint32_t codeword(uint32_t d) {
+    uint32_t lo, hi;
+    encode_cw<M>(d, 0u, lo, hi);
+    if constexpr (EXT) return (lo & ~1u) | (static_cast<uint32_t>(__popc(lo & ~1u)) & 1u);
+    else return lo >> 1;
+  }
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    uint32_t* T = reinterpret_cast<uint32_t*>(sh);
+    for (int e = tid; e < ENTRIES * 32; e += nth) {
+      const uint32_t x = static_cast<uint32_t>(e >> 5);
+      if constexpr (M == 3) T[e] = codeword(x & 0xFu) | (codeword(x >> 4) << CW_BITS);  // a pair
+      else T[e] = x < 64 ? codeword(x) : codeword((x - 64) << 6);
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&)[8], uint64_t, int, const Args&, const uint8_t* sh) {
+    uint32_t w[k];
+#pragma unroll
+    for (int i = 0; i < k; ++i) w[i] = in[i];
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    uint32_t o[OUT_W];
+#pragma unroll
+    for (int i = 0; i < OUT_W; ++i) o[i] = 0;
+    if constexpr (M == 3) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {  // codewords 2q, 2q+1 = data byte q
+        const uint32_t off = (((w[q >> 2] >> (8 * (q & 3))) & 0xFFu) << 7) | lane4;
+        put_bits(o, 2 * q * CW_BITS, *reinterpret_cast<const uint32_t*>(sh + off), 2 * CW_BITS);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const uint32_t d = take_bits(w, c * k) & 0x7FFu;
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(sh + (((d & 63u) << 7) | lane4)) ^
+                           *reinterpret_cast<const uint32_t*>(sh + ((((d >> 6) + 64u) << 7) | lane4));
+        put_bits(o, c * CW_BITS, v, CW_BITS);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
+  }
+};
+
 // splitmix64 output function (Steele, Lea & Flood 2014) -- written here
 // independently of oracle/oracle.c; the two are compared byte for byte.
 __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
@@ -1547,6 +1614,35 @@ hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_
                          corrected_dev, static_cast<cudaStream_t>(stream), false);
 }
 
+// encoder launch shapes (warps x stages), tunable with -D (tools/tune_shapes.py encode)
+#ifndef HAM_ENC_W3
+#define HAM_ENC_W3 16
+#define HAM_ENC_S3 8
+#endif
+#ifndef HAM_ENC_W4
+#define HAM_ENC_W4 16
+#define HAM_ENC_S4 4
+#endif
+#ifndef HAM_ENC_W5
+#define HAM_ENC_W5 12
+#define HAM_ENC_S5 3
+#endif
+#ifndef HAM_SENC_W3
+#define HAM_SENC_W3 16
+#define HAM_SENC_S3 8
+#endif
+#ifndef HAM_SENC_W4
+#define HAM_SENC_W4 16
+#define HAM_SENC_S4 3
+#endif
+#ifndef HAM_SENC_W5
+#define HAM_SENC_W5 8
+#define HAM_SENC_S5 3
+#endif
+#ifndef HAM_SENC_W6
+#define HAM_SENC_W6 6
+#define HAM_SENC_S6 2
+#endif
 hamming_status hamming_encode(int m, const void* data_dev, uint64_t N, void* rx_dev, void* stream) {
   g_launches = 0;
   g_grid = 0;
@@ -1562,15 +1658,11 @@ hamming_status hamming_encode(int m, const void* data_dev, uint64_t N, void* rx_
   const uint8_t* in = static_cast<const uint8_t*>(data_dev);
   uint8_t* out = static_cast<uint8_t*>(rx_dev);
   switch (m) {
-#define HAMMING_ENCODE_CASE(MM) \
-  case MM:                      \
-    return Launcher<EncodeOp<MM>, Shape<MM>::W, Shape<MM>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    HAMMING_ENCODE_CASE(2)
-    HAMMING_ENCODE_CASE(3)
-    HAMMING_ENCODE_CASE(4)
-    HAMMING_ENCODE_CASE(5)
-    HAMMING_ENCODE_CASE(6)
-#undef HAMMING_ENCODE_CASE
+    case 2: return Launcher<EncodeOp<2>, Shape<2>::W, Shape<2>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 3: return Launcher<EncodeLutOp<3>, HAM_ENC_W3, HAM_ENC_S3>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 4: return Launcher<EncodeLutOp<4>, HAM_ENC_W4, HAM_ENC_S4>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 5: return Launcher<EncodeOp<5>, HAM_ENC_W5, HAM_ENC_S5>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 6: return Launcher<EncodeOp<6>, Shape<6>::W, Shape<6>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_encode: m must be in [2, 6]");
 }
@@ -1757,14 +1849,10 @@ hamming_status hamming_encode_secded(int m, const void* data_dev, uint64_t N, vo
   const uint8_t* in = static_cast<const uint8_t*>(data_dev);
   uint8_t* out = static_cast<uint8_t*>(rx_dev);
   switch (m) {
-#define HAMMING_SECDED_ENC(MM) \
-  case MM:                     \
-    return Launcher<EncodeOp<MM, true>, 4, 2, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    HAMMING_SECDED_ENC(3)
-    HAMMING_SECDED_ENC(4)
-    HAMMING_SECDED_ENC(5)
-    HAMMING_SECDED_ENC(6)
-#undef HAMMING_SECDED_ENC
+    case 3: return Launcher<EncodeLutOp<3, true>, HAM_SENC_W3, HAM_SENC_S3, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 4: return Launcher<EncodeLutOp<4, true>, HAM_SENC_W4, HAM_SENC_S4, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 5: return Launcher<EncodeOp<5, true>, HAM_SENC_W5, HAM_SENC_S5, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 6: return Launcher<EncodeOp<6, true>, HAM_SENC_W6, HAM_SENC_S6, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_encode_secded: m must be in [3, 6]");
 }

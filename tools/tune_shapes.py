@@ -18,6 +18,14 @@ VARIANTS = {
 }
 
 
+ENCODE_VARIANTS = {
+    ("ENC", 3): [(16, 4), (8, 8), (16, 8), (24, 4)],
+    ("ENC", 4): [(8, 8), (16, 4), (12, 4), (8, 4)],
+    ("SENC", 3): [(8, 4), (16, 4), (16, 8)],
+    ("SENC", 4): [(8, 4), (16, 3), (8, 8)],
+    ("SENC", 5): [(8, 3), (12, 2), (4, 4)],
+    ("SENC", 6): [(4, 2), (8, 2), (6, 2)],
+}
 SECDED_VARIANTS = {
     3: [(16, 8), (8, 12), (16, 4), (24, 4)],
     4: [(8, 8), (16, 3), (12, 4), (8, 12), (16, 4)],
@@ -44,6 +52,9 @@ def build():
             # the other m keep their defaults
             defs = [f"HAM_W{m}={v[0]}", f"HAM_S{m}={v[1]}", f"HAM_IP{m}={'true' if v[2] else 'false'}"]
             jobs.append((os.path.join(OUT, name(m, v) + ".so"), defs))
+    if len(sys.argv) > 2 and sys.argv[2] == "encode":
+        jobs = [(os.path.join(OUT, f"enc_{nm}{m}_w{w}_s{st}.so"), [f"HAM_{nm}_W{m}={w}", f"HAM_{nm}_S{m}={st}"])
+                for (nm, m), vs in ENCODE_VARIANTS.items() for w, st in vs]
     if len(sys.argv) > 2 and sys.argv[2] == "secded":
         jobs = [(os.path.join(OUT, f"sec_m{m}_w{w}_s{st}.so"), [f"HAM_SEC_W{m}={w}", f"HAM_SEC_S{m}={st}"])
                 for m, vs in SECDED_VARIANTS.items() for w, st in vs]
@@ -57,6 +68,13 @@ def build():
 
 
 def run():
+    if len(sys.argv) > 2 and sys.argv[2] == "encode":
+        for (nm, m), vs in ENCODE_VARIANTS.items():
+            for w, st in vs:
+                env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"enc_{nm}{m}_w{w}_s{st}.so"))
+                print(nm, m, w, st, flush=True)
+                subprocess.run([sys.executable, os.path.join(ROOT, "tools", "encode_bench.py"), "--m", str(m)], env=env)
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "secded":
         for m, vs in SECDED_VARIANTS.items():
             for w, st in vs:
