@@ -352,9 +352,6 @@ struct BatchGeom {
 hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
-  const uint32_t chunks = (maxn + 32) / 32;
-  uint32_t L = 1;
-  while (L < 32 && L * 8 < chunks) L *= 2;
 #ifndef HAM_PKT_BUDGET
 #define HAM_PKT_BUDGET (6 * 1024)
 #endif
@@ -363,6 +360,21 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   uint64_t G = budget > 96 ? (budget - 96) / per : 1;
   G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
   b.G = static_cast<uint32_t>(G);
+  // lanes per item in pass S: the L minimising an issue-count model of the pass --
+  // ceil(items / (32 / L)) rounds, each a fixed set-up + epilogue (~90 warp
+  // instructions, + 4 per shuffle step) and ceil(C64 / 4L) unrolled blocks of
+  // ~42 -- so short codewords and many items per batch take small groups
+  const uint32_t items = static_cast<uint32_t>(G) * g.t, c64 = (maxn + 1) / 64 + 1;
+  uint32_t L = 1;
+  uint64_t best = ~0ull;
+  for (uint32_t l = 1, lg = 0; l <= 32; l *= 2, ++lg) {
+    const uint64_t rounds = (items + 32 / l - 1) / (32 / l);
+    const uint64_t cost = rounds * (90 + 4 * (l == 32 ? 0 : lg) + 42 * ((c64 + 4 * l - 1) / (4 * l)));
+    if (cost < best) best = cost, L = l;
+  }
+#ifdef HAM_PKT_L
+  L = HAM_PKT_L;
+#endif
   b.L = L;
   b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
   b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
