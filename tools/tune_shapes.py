@@ -32,7 +32,7 @@ SECDED_VARIANTS = {
     5: [(12, 3), (8, 4), (16, 2), (8, 3)],
     6: [(8, 3), (12, 2), (8, 2)],
 }
-PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((5120, 2, 1, 16), (7168, 2, 1, 16), (6144, 2, 1, 12), (8192, 2, 1, 12), (4096, 2, 1, 32), (5120, 2, 1, 24), (6144, 2, 1, 20))]
+PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((4096, 2, 1, 16), (6144, 2, 1, 16), (8192, 2, 1, 16), (10240, 2, 1, 16), (8192, 2, 1, 8), (12288, 2, 1, 8), (4096, 2, 1, 32))]
 
 
 def name(m, v):
