@@ -102,3 +102,38 @@ def test_longest_segments_roundtrip(M, t):
     torch.cuda.synchronize()
     assert torch.equal(res.messages[: P * M], msg[: P * M])
     assert (res.status[:P] == 1).all() and res.counts.cpu().tolist() == [P * t, 0]
+
+
+def _random_geometries(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        M = int(rng.choice([int(rng.integers(1, 64)), int(rng.integers(64, 1100)), int(rng.integers(1100, 4097))]))
+        t = int(rng.integers(1, 17))
+        if 8 * M < t:
+            continue
+        k0, n0 = ham.packet_layout(M, t)
+        if max(n0) > 16384:      # the oracle's segment limit (larger ones: test_longest_segments_roundtrip)
+            continue
+        out.append((M, t, int(rng.integers(0, 3))))
+    return out
+
+
+@pytest.mark.parametrize("M,t,extra", _random_geometries(40, 0x9E0))
+def test_random_geometries_strides_and_batches(oracle, M, t, extra):
+    """Seeded random (M, t) over the whole accepted range, a received-packet
+    stride padded by 0..2 extra 16-byte slots, random received bits plus
+    encoded packets with single errors, a packet count that leaves a ragged
+    last batch: messages, syndromes, statuses and counts equal the oracle's."""
+    stride = ham.packet_stride(M, t) + 16 * extra
+    P = 37 + 5 * extra
+    rng = np.random.default_rng(M * 131 + t)
+    rx, _ = oracle.generate_packets(M, t, 0xA11 + M, 0, P, stride, p=0.8, want_msg=True)
+    noise = rng.integers(0, 256, P * stride, dtype=np.uint8)
+    mix = np.where(np.repeat(rng.random(P) < 0.3, stride), noise, rx).astype(np.uint8)
+    wm, ws, wst = oracle.decode_packets(M, t, mix, P, stride)
+    gm, gs, gst, cnt = gpu_decode(M, t, mix, P, stride)
+    assert np.array_equal(gm, wm) and np.array_equal(gs, ws) and np.array_equal(gst, wst)
+    k, n = ham.packet_layout(M, t)
+    n = np.array(n)
+    assert cnt.tolist() == [int(((ws > 0) & (ws <= n)).sum()), int((ws > n).sum())]
