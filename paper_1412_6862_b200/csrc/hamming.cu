@@ -134,6 +134,19 @@ __device__ __forceinline__ void tensor_g2s_3d(void* dst, const void* tmap, int x
       "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
+// TMA tensor stores (shared -> global through a tensor map), bulk-group completion.
+__device__ __forceinline__ void tensor_s2g_2d(const void* tmap, int x, int y, const void* src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   tmap),
+               "r"(x), "r"(y), "r"(smem_addr(src)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void tensor_s2g_3d(const void* tmap, int x, int y, int z, const void* src, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(tmap),
+      "r"(x), "r"(y), "r"(z), "r"(smem_addr(src)), "l"(pol)
+      : "memory");
+}
 // 1-D TMA: shared -> global, bulk-group completion.
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
@@ -839,7 +852,15 @@ struct EncodeOp {
   static constexpr bool HAS_SIDE = false;
   static constexpr int NCOUNT = 1;
   static constexpr int SHARED = 0;
-  struct Args {};
+  // SECDED (32,26) / (64,57) output: a lane's 2^m-word stride would put every
+  // lane's stores in the same banks, so the tile is written through the
+  // swizzle (swz_unit) and stored by a tensor map.
+  static constexpr bool SWZ_OUT = EXT && M >= 5;
+  struct NoArgs {};
+  struct OutArgs {
+    CUtensorMap tmap_out;
+  };
+  using Args = typename std::conditional<SWZ_OUT, OutArgs, NoArgs>::type;
   __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -866,8 +887,16 @@ struct EncodeOp {
       if constexpr (EXT) put_ext_codeword<M>(o, c * CW_BITS, lo, hi);
       else put_codeword<M>(o, c * n, lo, hi);
     }
+    if constexpr (SWZ_OUT) {  // `out` is the output tile base
+      const uint32_t l = threadIdx.x & 31u;
 #pragma unroll
-    for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
+      for (int u = 0; u < OUT_W / 4; ++u)
+        reinterpret_cast<uint4*>(out - l * OUT_W)[swz_unit<OUT_W>(l * (OUT_W / 4) + u)] =
+            make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
+    }
     (void)n;
   }
 };
@@ -1034,11 +1063,29 @@ struct Swizzled<Op, decltype(void(Op::SWZ))> {
   static constexpr bool value = Op::SWZ;
 };
 
+template <class Op, class = void>
+struct SwizzledOut {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct SwizzledOut<Op, decltype(void(Op::SWZ_OUT))> {
+  static constexpr bool value = Op::SWZ_OUT;
+};
+
 template <class Op>
 struct TileBytes {
   static constexpr int IN = Op::IN_W * 128;   // 32 lanes x IN_W words x 4 B
   static constexpr int OUT = Op::OUT_W * 128;
   static constexpr bool SWZ = Swizzled<Op>::value;
+  // output tiles written through the same swizzle and stored by a tensor map
+  static constexpr bool SWZ_OUT = SwizzledOut<Op>::value;
+  __host__ __device__ static constexpr uint32_t staged_out(uint32_t i) {
+    if constexpr (SWZ_OUT) {
+      return (swz_unit<Op::OUT_W>(i >> 4) << 4) | (i & 15u);
+    } else {
+      return i;
+    }
+  }
   // shared-memory byte offset of tile byte i (128-byte swizzle for SWZ tiles)
   __host__ __device__ static constexpr uint32_t staged(uint32_t i) {
     if constexpr (SWZ) {
@@ -1104,11 +1151,12 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
   const uint64_t ob0 = tile * OUT;
   const uint64_t nbo = out_total - ob0;
   const uint8_t* ob = reinterpret_cast<const uint8_t*>(obuf);
-  for (int i = lane * 16; static_cast<uint64_t>(i) < nbo; i += 512) {
+  for (int i = lane * 16; static_cast<uint64_t>(i) < nbo; i += 512) {  // 16-byte units, un-swizzled
+    const uint8_t* srcu = ob + TileBytes<Op>::staged_out(static_cast<uint32_t>(i));
     if (static_cast<uint64_t>(i) + 16 <= nbo) {
-      *reinterpret_cast<uint4*>(out + ob0 + i) = *reinterpret_cast<const uint4*>(ob + i);
+      *reinterpret_cast<uint4*>(out + ob0 + i) = *reinterpret_cast<const uint4*>(srcu);
     } else {
-      for (int b = 0; static_cast<uint64_t>(i + b) < nbo; ++b) out[ob0 + i + b] = ob[i + b];
+      for (int b = 0; static_cast<uint64_t>(i + b) < nbo; ++b) out[ob0 + i + b] = srcu[b];
     }
   }
   uint32_t cnt = 0;
@@ -1137,9 +1185,14 @@ struct TileLayout {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
   static constexpr bool IN_PLACE = WANT_IN_PLACE && IN > 0 && OUT <= IN;
   static constexpr int OUT_BUFS = IN_PLACE ? 0 : 2;
-  // swizzled stages stay 1024-byte aligned from warp to warp
+  static constexpr bool ALIGN1K = TileBytes<Op>::SWZ || TileBytes<Op>::SWZ_OUT;
+  // byte offset of the output buffers (after the input stages)
+  __host__ __device__ static constexpr int out_off(int stages) {
+    return ALIGN1K ? (stages * IN + 1023) / 1024 * 1024 : stages * IN;
+  }
+  // swizzled buffers stay 1024-byte aligned from warp to warp
   __host__ __device__ static constexpr int warp_bytes(int stages) {
-    return TileBytes<Op>::SWZ ? (stages * IN + OUT_BUFS * OUT + 1023) / 1024 * 1024 : stages * IN + OUT_BUFS * OUT;
+    return ALIGN1K ? (out_off(stages) + OUT_BUFS * OUT + 1023) / 1024 * 1024 : stages * IN + OUT_BUFS * OUT;
   }
 };
 
@@ -1159,7 +1212,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   uint8_t* const sh = smem;  // Op::SHARED bytes of CTA-wide tables first
   // 128-byte-swizzled TMA destinations must be 1024-byte aligned
   uint8_t* const tiles = smem + Op::SHARED +
-                         (TileBytes<Op>::SWZ ? ((1024u - (smem_addr(smem + Op::SHARED) & 1023u)) & 1023u) : 0u);
+                         ((TileBytes<Op>::SWZ || TileBytes<Op>::SWZ_OUT)
+                              ? ((1024u - (smem_addr(smem + Op::SHARED) & 1023u)) & 1023u)
+                              : 0u);
   uint8_t* wbase = tiles + warp * WARP_SMEM;
   uint64_t* bars = reinterpret_cast<uint64_t*>(tiles + WARPS * WARP_SMEM) + warp * STAGES;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
@@ -1195,7 +1250,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       obuf = reinterpret_cast<uint32_t*>(wbase + st * IN);
     } else {
       if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
-      obuf = reinterpret_cast<uint32_t*>(wbase + STAGES * IN + (it & 1u) * OUT);
+      obuf = reinterpret_cast<uint32_t*>(wbase + TL::out_off(STAGES) + (it & 1u) * OUT);
       if (lane == 0) bulk_wait_read<1>();  // the store issued two tiles ago has read obuf
       __syncwarp();
     }
@@ -1206,7 +1261,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
     __syncwarp();
     if (lane == 0) {
-      bulk_s2g(out + t * OUT, obuf, OUT, pol);
+      if constexpr (TileBytes<Op>::SWZ_OUT) {
+        if constexpr (Op::OUT_W / 32 >= 2) tensor_s2g_3d(&args.tmap_out, 0, static_cast<int>(t * 32), 0, obuf, pol);
+        else tensor_s2g_2d(&args.tmap_out, 0, static_cast<int>(t * (OUT / 128)), obuf, pol);
+      } else {
+        bulk_s2g(out + t * OUT, obuf, OUT, pol);
+      }
       bulk_commit();
       if constexpr (TL::IN_PLACE) {
         // refill the stage of the PREVIOUS tile: its in-place store was issued a
@@ -1238,7 +1298,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   if (rem > 0 && gw == n_full % nw) {  // the ragged tail tile
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
-    uint8_t* tail_out = TL::IN_PLACE ? wbase : wbase + STAGES * IN;
+    uint8_t* tail_out = TL::IN_PLACE ? wbase : wbase + TL::out_off(STAGES);
     cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
                              reinterpret_cast<uint32_t*>(tail_out), lane, args, sh, cnt2);
   }
@@ -1289,7 +1349,7 @@ int sm_count(int dev) {
 template <class Op, int WARPS, int STAGES, bool INPLACE = true>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
-  static constexpr size_t SMEM = Op::SHARED + (TileBytes<Op>::SWZ ? 1024 : 0) +
+  static constexpr size_t SMEM = Op::SHARED + ((TileBytes<Op>::SWZ || TileBytes<Op>::SWZ_OUT) ? 1024 : 0) +
                                  static_cast<size_t>(WARPS) * TileLayout<Op, INPLACE>::warp_bytes(STAGES) +
                                  WARPS * STAGES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -1397,6 +1457,15 @@ hamming_status run_swizzled(const uint8_t* in, uint8_t* out, uint8_t* side, uint
   const hamming_status s = make_tile_tmap(&a.tmap, in, N / kTileCw, TileBytes<Op>::IN);
   if (s != HAMMING_OK) return s;
   return Launcher<Op, WARPS, STAGES, true>::run(in, out, side, N, ib, ob, counter, a, st);
+}
+
+template <class Op, int WARPS, int STAGES>
+hamming_status run_swizzled_out(const uint8_t* in, uint8_t* out, uint64_t N, uint64_t ib, uint64_t ob,
+                                cudaStream_t st) {
+  typename Op::Args a;
+  const hamming_status s = make_tile_tmap(&a.tmap_out, out, N / kTileCw, TileBytes<Op>::OUT);
+  if (s != HAMMING_OK) return s;
+  return Launcher<Op, WARPS, STAGES, false>::run(in, out, nullptr, N, ib, ob, nullptr, a, st);
 }
 
 bool ranges_overlap(const void* a, uint64_t na, const void* b, uint64_t nb) {
@@ -1851,8 +1920,8 @@ hamming_status hamming_encode_secded(int m, const void* data_dev, uint64_t N, vo
   switch (m) {
     case 3: return Launcher<EncodeLutOp<3, true>, HAM_SENC_W3, HAM_SENC_S3, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
     case 4: return Launcher<EncodeLutOp<4, true>, HAM_SENC_W4, HAM_SENC_S4, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    case 5: return Launcher<EncodeOp<5, true>, HAM_SENC_W5, HAM_SENC_S5, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    case 6: return Launcher<EncodeOp<6, true>, HAM_SENC_W6, HAM_SENC_S6, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 5: return run_swizzled_out<EncodeOp<5, true>, HAM_SENC_W5, HAM_SENC_S5>(in, out, N, ib, ob, st);
+    case 6: return run_swizzled_out<EncodeOp<6, true>, HAM_SENC_W6, HAM_SENC_S6>(in, out, N, ib, ob, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_encode_secded: m must be in [3, 6]");
 }
