@@ -1217,7 +1217,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                               : 0u);
   uint8_t* wbase = tiles + warp * WARP_SMEM;
   uint64_t* bars = reinterpret_cast<uint64_t*>(tiles + WARPS * WARP_SMEM) + warp * STAGES;
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
+  // global warp index, CTA-minor: the last, partial round of tiles (n_full % nw
+  // of them) lands on one warp of as many different SMs as possible rather
+  // than on every warp of the first few CTAs
+  const uint64_t gw = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
 

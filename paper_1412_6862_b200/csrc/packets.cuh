@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t n_batches = (a.n_packets + bg.G - 1) / bg.G;
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPktWarps + warp;
+  const uint64_t gw = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x;  // CTA-minor (see tiles_kernel)
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
   const uint64_t pol = policy_evict_first();
   const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
