@@ -478,23 +478,25 @@ __device__ __forceinline__ uint32_t insert_byte1(uint32_t word, uint32_t e, int 
   return __byte_perm(word, e, sel);
 }
 
-// (7,4): per-lane replicated 128-entry table, entry = data (bits 0..3) |
-// syndrome << 8; lane l reads word [x][l], always its own bank (16 KB).
+// (7,4): per-lane replicated 128-entry table of 8-byte entries {data nibble
+// replicated into all eight nibbles, syndrome}; lane l reads entry [x][l],
+// always its own bank pair (32 KB).  The replicated nibble goes to its place
+// in the output word with one LOP3 against a constant mask (no shift).
 struct DecodeLut3Op {
   static constexpr int NCOUNT = 1;
   __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
   static constexpr bool HAS_SIDE = true;
-  static constexpr int SHARED = 128 * 32 * 4;
+  static constexpr int SHARED = 128 * 32 * 8;
   struct Args {};
 
   __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
-    uint32_t* L = reinterpret_cast<uint32_t*>(sh);
+    uint2* L = reinterpret_cast<uint2*>(sh);
     for (int e = tid; e < 128 * 32; e += nth) {
       uint32_t dlo, dhi;
       const uint32_t s = decode_cw<3>(static_cast<uint32_t>(e >> 5) << 1, 0u, dlo, dhi);
-      L[e] = dlo | (s << 8);
+      L[e] = make_uint2(dlo * 0x11111111u, s);
     }
   }
 
@@ -505,15 +507,14 @@ struct DecodeLut3Op {
 #pragma unroll
     for (int i = 0; i < 7; ++i) w[i] = in[i];
     __syncwarp();  // every lane has its input words: the tile may be overwritten in place
-    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    const uint32_t lane8 = (threadIdx.x & 31u) << 3;
     uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const uint32_t off = (field_at(w, 7 * c, 7) & 0x3F80u) | lane4;  // (x * 32 + lane) * 4
-      const uint32_t e = *reinterpret_cast<const uint32_t*>(sh + off);
-      const int r = (4 * c) & 31;
-      o[c >> 3] |= (e << r) & (0xFu << r);
-      side[c >> 2] = insert_byte1(side[c >> 2], e, c & 3);
+      const uint32_t off = (field_at(w, 7 * c, 8) & 0x7F00u) | lane8;  // (x * 32 + lane) * 8
+      const uint2 e = *reinterpret_cast<const uint2*>(sh + off);
+      o[c >> 3] |= e.x & (0xFu << ((4 * c) & 31));
+      side[c >> 2] |= e.y << (8 * (c & 3));
     }
     *reinterpret_cast<uint4*>(out) = make_uint4(o[0], o[1], o[2], o[3]);
   }
@@ -667,14 +668,15 @@ __device__ __forceinline__ uint32_t secded_flags(uint32_t s, uint32_t par) {
   return s | (par << 6) | ((static_cast<uint32_t>(s != 0) & (par ^ 1u)) << 7);
 }
 
-// (8,4): a codeword is one byte; per-lane replicated 256-entry table (32 KB),
-// entry = final data nibble (bits 0..3) | flags << 8.
+// (8,4): a codeword is one byte; per-lane replicated 256-entry table of 8-byte
+// entries {final data nibble replicated into all eight nibbles, flags} (64 KB),
+// placed as in DecodeLut3Op.
 struct DecodeSecded3Op {
   static constexpr int NCOUNT = 2;
   static constexpr int IN_W = 8, OUT_W = 4, IN_BITS = 8;
   static constexpr bool HAS_SIDE = true;
   static constexpr bool SWZ = true;
-  static constexpr int SHARED = 256 * 32 * 4;
+  static constexpr int SHARED = 256 * 32 * 8;
   struct Args {
     CUtensorMap tmap;
   };
@@ -692,14 +694,14 @@ struct DecodeSecded3Op {
   }
 
   __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
-    uint32_t* L = reinterpret_cast<uint32_t*>(sh);
+    uint2* L = reinterpret_cast<uint2*>(sh);
     for (int e = tid; e < 256 * 32; e += nth) {
       uint32_t v = static_cast<uint32_t>(e >> 5);  // bit p = position p, bit 0 = P
       const uint32_t s = syndrome_cw<3>(v, 0u);
       const uint32_t par = static_cast<uint32_t>(__popc(v)) & 1u;
       v ^= par << s;
       const uint32_t d = ((v >> 3) & 1u) | ((v >> 4) & 0xEu);  // positions 3, 5, 6, 7
-      L[e] = d | (secded_flags(s, par) << 8);
+      L[e] = make_uint2(d * 0x11111111u, secded_flags(s, par));
     }
   }
 
@@ -709,15 +711,16 @@ struct DecodeSecded3Op {
     uint32_t w[8];
     load_swizzled<8>(in, w);
     __syncwarp();  // every lane has its input words: the tile may be overwritten in place
-    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    const uint32_t lane8 = (threadIdx.x & 31u) << 3;
     uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      const uint32_t off = (((w[c >> 2] >> (8 * (c & 3))) & 0xFFu) << 7) | lane4;  // (x * 32 + lane) * 4
-      const uint32_t e = *reinterpret_cast<const uint32_t*>(sh + off);
-      const int r = (4 * c) & 31;
-      o[c >> 3] |= (e & 0xFu) << r;
-      side[c >> 2] = insert_byte1(side[c >> 2], e, c & 3);
+      // (x * 32 + lane) * 8 with x = byte c of the lane's words
+      const int bo = 8 * (c & 3);
+      const uint32_t off = ((bo <= 8 ? (w[c >> 2] << (8 - bo)) : (w[c >> 2] >> (bo - 8))) & 0xFF00u) | lane8;
+      const uint2 e = *reinterpret_cast<const uint2*>(sh + off);
+      o[c >> 3] |= e.x & (0xFu << ((4 * c) & 31));
+      side[c >> 2] |= e.y << bo;
     }
     *reinterpret_cast<uint4*>(out) = make_uint4(o[0], o[1], o[2], o[3]);
   }
