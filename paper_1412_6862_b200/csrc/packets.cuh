@@ -279,6 +279,8 @@ struct PacketTables {
   uint32_t Wp;                    // message words per packet, ceil(msg_bytes / 4)
   uint32_t n_special, n_pieces;
   uint32_t mag_t, mag_ns, mag_wp, mag_np;  // floor(2^32 / d), d = t, n_special, Wp, n_pieces (divmod_small)
+  uint32_t headx;                 // 1: segment heads are compacted in place first (pass X, kPktHeadxMinK)
+  uint32_t Wfull, rem, mag_rem;   // pass R: Wp = Wfull + rem, Wfull a multiple of 32; floor(2^32 / rem)
   // src0 (bits 0..15) | nb0 (bits 16..21): a word is slice 0 (nb0 bits) and, if nb0 < 32, slice 1 =
   // the stream one bit after slice 0 ends (a skipped parity position); head words: 32 << 16
   uint32_t word0[kPktMaxWords];
@@ -296,9 +298,17 @@ uint32_t host_run_of(uint32_t d) {
   return j;
 }
 
+// Pass X (heads compacted in place) needs every segment's 57-bit head window
+// (positions 7..63) at least 32 bits clear of the next segment's, so that no
+// two lanes rewrite the same stream word: k >= 96 gives n >= 103.
+constexpr uint32_t kPktHeadxMinK = 96;
+
 hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
   const uint32_t bits = g.msg_bytes * 8u;
   T.Wp = (g.msg_bytes + 3) / 4;
+  uint32_t kmin = ~0u;
+  for (uint32_t i = 0; i < g.t; ++i) kmin = std::min(kmin, g.k[i]);
+  T.headx = kmin >= kPktHeadxMinK ? 1u : 0u;
   T.n_special = 0;
   T.n_pieces = 0;
   uint32_t seg = 0;
@@ -309,6 +319,15 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
     while (d < dend) {
       while (d >= g.moff[seg] + g.k[seg]) ++seg;
       const uint32_t dl = d - g.moff[seg];
+      if (T.headx && dl < 57) {  // after pass X: data bits 0..56 at positions 7..63, contiguous
+        const uint32_t take = std::min(57u - dl, dend - d);
+        src[np] = g.off[seg] + dl + 6;
+        len[np] = take;
+        pos[np] = d - 32u * W;
+        ++np;
+        d += take;
+        continue;
+      }
       const uint32_t j = host_run_of(dl);
       const uint32_t run_end = std::min((2u << j) - j - 2, g.k[seg]);
       const uint32_t take = std::min(run_end - dl, dend - d);
@@ -337,6 +356,9 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
   T.mag_ns = mag(T.n_special);
   T.mag_wp = mag(T.Wp);
   T.mag_np = mag(T.n_pieces);
+  T.Wfull = T.Wp / 32 * 32;
+  T.rem = T.Wp - T.Wfull;
+  T.mag_rem = mag(T.rem);
   return HAMMING_OK;
 }
 
@@ -459,7 +481,7 @@ __device__ __forceinline__ uint32_t divmod_small(uint32_t u, uint32_t d, uint32_
   return q;
 }
 
-template <uint32_t L>
+template <uint32_t L, bool HX>
 __global__ void __launch_bounds__(kPktWarps * 32)
     packets_decode_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ BatchGeom bg,
                           const __grid_constant__ PacketArgs a, const __grid_constant__ PacketTables T) {
@@ -528,6 +550,42 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
     mbar_wait(&bars[buf], (it / kPktStages) & 1u);
     __syncwarp();
+    {  // pass S: syndromes per (packet, segment) item, by groups of L lanes (reads the stream as received)
+      const uint32_t items = np * g.t;
+      for (uint32_t base = 0; base < items; base += groups) {
+        const bool active = base + gid < items;
+        uint32_t seg;
+        const uint32_t pk = divmod_small(active ? base + gid : 0, g.t, T.mag_t, seg);
+        const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
+        const uint32_t off = pk * stride_bits + sg[seg];
+        const uint32_t s = group_syndrome64<L>(w, off, n, active, q);
+        if (active && q == 0) sbuf[base + gid] = s;
+      }
+    }
+    if constexpr (HX) {  // pass X: compact each segment's head in place (RR of positions 0..63)
+      __syncwarp();
+      uint32_t* wm = const_cast<uint32_t*>(w);
+      for (uint32_t i = lane; i < np * g.t; i += 32) {
+        uint32_t seg;
+        const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
+        const uint32_t o = pk * stride_bits + sg[seg] + kPadBits - 1;  // buffer bit of position 0
+        uint32_t* wq = wm + (o >> 5);
+        const uint32_t r = o & 31u;
+        const uint32_t w0 = wq[0], w1 = wq[1], w2 = wq[2];
+        const uint64_t x = static_cast<uint64_t>(__funnelshift_r(w0, w1, r)) |
+                           (static_cast<uint64_t>(__funnelshift_r(w1, w2, r)) << 32);  // bit p = position p
+        // data positions 3, 5..7, 9..15, 17..31, 33..63 -> bits 0..56 (the m = 6 compaction, App. A)
+        const uint64_t d = ((x >> 3) & 0x1ull) | ((x >> 4) & 0xeull) | ((x >> 5) & 0x7f0ull) |
+                           ((x >> 6) & 0x3fff800ull) | ((x >> 7) & 0x1fffffffc000000ull);
+        const uint64_t xn = (x & 0x7full) | (d << 7);  // positions 0..6 kept, data at 7..63
+        const uint32_t lo = static_cast<uint32_t>(xn), hi = static_cast<uint32_t>(xn >> 32);
+        const uint32_t lm = (1u << r) - 1u;
+        wq[0] = (w0 & lm) | (lo << r);
+        wq[1] = __funnelshift_l(lo, hi, r);
+        wq[2] = (w2 & ~lm) | __funnelshift_l(hi, 0u, r);
+      }
+    }
+    __syncwarp();
     {  // pass R: every word as one or two slices (lane: word W of every packet of the batch)
       const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
       if (np == 1) {  // one packet per batch (long packets): no inner loop
@@ -536,15 +594,26 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
           mbuf[W] = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
         }
-      } else
-      for (uint32_t W = lane; W < Wp; W += 32) {
-        const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
-        const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
-        uint32_t* mp = mbuf + W;
-        for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
+      } else {
+        for (uint32_t W = lane; W < T.Wfull; W += 32) {
+          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
+          const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
+          uint32_t* mp = mbuf + W;
+          for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
+            const uint32_t a0 = wp[0], a1 = wp[1];
+            // slice 1 is the stream one bit further on (the parity position skipped)
+            *mp = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+          }
+        }
+        // the last Wp mod 32 words of every packet, flattened over (packet, word)
+        for (uint32_t e = lane; e < np * T.rem; e += 32) {
+          uint32_t c;
+          const uint32_t p = divmod_small(e, T.rem, T.mag_rem, c);
+          const uint32_t W = T.Wfull + c;
+          const uint4 d = wdesc[W];
+          const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          // slice 1 is the stream one bit further on (the parity position skipped)
-          *mp = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+          mbuf[p * Wp + W] = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
         }
       }
     }
@@ -557,19 +626,6 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         const uint32_t s0 = kPadBits + p * stride_bits + (pc.x & 0xFFFFu), len = (pc.x >> 16) & 63u;
         const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
         atomicOr(&mbuf[p * Wp + pc.y], x << ((pc.x >> 24) & 31u));
-      }
-    }
-    __syncwarp();
-    {  // pass S: syndromes per (packet, segment) item, by groups of L lanes
-      const uint32_t items = np * g.t;
-      for (uint32_t base = 0; base < items; base += groups) {
-        const bool active = base + gid < items;
-        uint32_t seg;
-        const uint32_t pk = divmod_small(active ? base + gid : 0, g.t, T.mag_t, seg);
-        const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
-        const uint32_t off = pk * stride_bits + sg[seg];
-        const uint32_t s = group_syndrome64<L>(w, off, n, active, q);
-        if (active && q == 0) sbuf[base + gid] = s;
       }
     }
     __syncwarp();
@@ -657,14 +713,21 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   const size_t smem = bg.tab_bytes + static_cast<size_t>(kPktWarps) * bg.warp_bytes;
   if (smem > 227 * 1024) return set_err(HAMMING_E_ARG, "packets: shared memory budget exceeded");
   void (*kfn)(PacketGeom, BatchGeom, PacketArgs, PacketTables) = nullptr;
-  switch (bg.L) {
-    case 1: kfn = packets_decode_kernel<1>; break;
-    case 2: kfn = packets_decode_kernel<2>; break;
-    case 4: kfn = packets_decode_kernel<4>; break;
-    case 8: kfn = packets_decode_kernel<8>; break;
-    case 16: kfn = packets_decode_kernel<16>; break;
-    default: kfn = packets_decode_kernel<32>; break;
+#define HAM_PKT_KFN(HX)                                   \
+  switch (bg.L) {                                         \
+    case 1: kfn = packets_decode_kernel<1, HX>; break;    \
+    case 2: kfn = packets_decode_kernel<2, HX>; break;    \
+    case 4: kfn = packets_decode_kernel<4, HX>; break;    \
+    case 8: kfn = packets_decode_kernel<8, HX>; break;    \
+    case 16: kfn = packets_decode_kernel<16, HX>; break;  \
+    default: kfn = packets_decode_kernel<32, HX>; break;  \
   }
+  if (T.headx) {
+    HAM_PKT_KFN(true)
+  } else {
+    HAM_PKT_KFN(false)
+  }
+#undef HAM_PKT_KFN
   e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets decode)");
   // ask for the full shared-memory carveout so several CTAs fit per SM

@@ -12,6 +12,9 @@ pytestmark = pytest.mark.gpu
 
 GRID = [(M, t) for M in (400, 800, 1200, 1600, 2000) for t in (2, 3, 4, 5, 6)]
 EDGE = [(1, 1), (1, 8), (13, 3), (16, 16), (1024, 1), (999, 7)]
+# around the in-place head compaction threshold (every k >= 96): (12,1) k=96, (72,6) k=96,
+# (71,6) k=94..95 (not compacted), (73,6) k=97..98, (97,8) k=97, (11,1) k=88
+HEADX = [(12, 1), (72, 6), (71, 6), (73, 6), (97, 8), (11, 1)]
 
 
 def gpu_decode(M, t, rx_np, P, stride):
@@ -33,7 +36,7 @@ def test_generator_matches_oracle(oracle, M, t):
     assert np.array_equal(gmsg.cpu().numpy()[: P * M], wmsg)
 
 
-@pytest.mark.parametrize("M,t", GRID + EDGE)
+@pytest.mark.parametrize("M,t", GRID + EDGE + HEADX)
 def test_decode_matches_oracle(oracle, M, t):
     stride = ham.packet_stride(M, t)
     P = 53
@@ -45,7 +48,7 @@ def test_decode_matches_oracle(oracle, M, t):
     assert cnt.tolist() == [int((ws > 0).sum()), 0]
 
 
-@pytest.mark.parametrize("M,t", [(400, 2), (400, 6), (2000, 2), (13, 3), (1, 1), (16, 16), (999, 7)])
+@pytest.mark.parametrize("M,t", [(400, 2), (400, 6), (2000, 2), (13, 3), (1, 1), (16, 16), (999, 7)] + HEADX)
 def test_random_received_packets(oracle, M, t):
     """Uniformly random received bits: many segments carry syndromes beyond
     n (uncorrectable) or miscorrect; GPU and oracle must agree exactly."""
