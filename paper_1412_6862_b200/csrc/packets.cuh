@@ -342,7 +342,7 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
     } else {
       if (T.n_special >= kPktMaxSpecial || T.n_pieces + np > kPktMaxPieces)
         return set_err(HAMMING_E_ARG, "packets: piece table overflow");
-      T.word0[W] = 33u << 16;  // head word: pass R writes 0, pass H ORs its pieces in
+      T.word0[W] = 33u << 16;  // head word: pass H overwrites what pass R stored
       T.special[T.n_special++] = W | (T.n_pieces << 16);
       for (uint32_t i = 0; i < np; ++i) {
         T.piece_word[T.n_pieces] = static_cast<uint16_t>(W);
@@ -403,7 +403,7 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
   b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
                  static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
-  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
+  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
   if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
     return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
   return HAMMING_OK;
@@ -489,18 +489,21 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   __shared__ unsigned long long cta_counts[2];
   __shared__ __align__(8) uint64_t bars_all[kPktWarps * kPktStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Wp = T.Wp, npc = T.n_pieces;
+  const uint32_t Wp = T.Wp, nsp = T.n_special;
   // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
   // pieces {src | len | pos, word}, per-segment geometry
   uint4* wdesc = reinterpret_cast<uint4*>(smem);
   uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * Wp);
-  uint32_t* sg = reinterpret_cast<uint32_t*>(pieces + T.n_pieces);  // [off | n | k | moff] x kPktMaxSeg
+  uint2* spec = pieces + T.n_pieces;  // head words {word, first piece | end piece << 16}
+  uint32_t* sg = reinterpret_cast<uint32_t*>(spec + T.n_special);  // [off | n | k | moff] x kPktMaxSeg
   for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
-    const bool head = nb > 32;  // head words are 0 after pass R and OR-ed together by pass H
+    const bool head = nb > 32;  // head words: pass H overwrites them
     wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, head ? 0u : 0xFFFFFFFFu);
   }
   for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = make_uint2(T.piece[i], T.piece_word[i]);
+  for (uint32_t i = threadIdx.x; i < T.n_special; i += blockDim.x)
+    spec[i] = make_uint2(T.special[i] & 0xFFFFu, (T.special[i] >> 16) | (T.special[i + 1] & 0xFFFF0000u));
   if (threadIdx.x < g.t) {
     sg[threadIdx.x] = g.off[threadIdx.x];
     sg[kPktMaxSeg + threadIdx.x] = g.n[threadIdx.x];
@@ -547,7 +550,9 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
     uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + (it % kPktMsgBufs) * bg.msg_cap);
     if (lane == 0) bulk_wait_read<kPktMsgBufs - 1>();  // the bulk store that last used this mbuf has read it
-    for (uint32_t i = lane; i < np; i += 32) pst[i] = 0;
+    // G <= 64: two predicated stores (a lane-strided loop here compiles to ~40 instructions of unroll set-up)
+    if (static_cast<uint32_t>(lane) < np) pst[lane] = 0;
+    if (static_cast<uint32_t>(lane) + 32 < np) pst[lane + 32] = 0;
     mbar_wait(&bars[buf], (it / kPktStages) & 1u);
     __syncwarp();
     {  // pass S: syndromes per (packet, segment) item, by groups of L lanes (reads the stream as received)
@@ -565,6 +570,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     if constexpr (HX) {  // pass X: compact each segment's head in place (RR of positions 0..63)
       __syncwarp();
       uint32_t* wm = const_cast<uint32_t*>(w);
+      #pragma unroll 1
       for (uint32_t i = lane; i < np * g.t; i += 32) {
         uint32_t seg;
         const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
@@ -592,20 +598,21 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         for (uint32_t W = lane; W < Wp; W += 32) {
           const uint4 d = wdesc[W];
           const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
-          mbuf[W] = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+          mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
         }
       } else {
         for (uint32_t W = lane; W < T.Wfull; W += 32) {
-          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
+          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, -}
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
           uint32_t* mp = mbuf + W;
           for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
             const uint32_t a0 = wp[0], a1 = wp[1];
             // slice 1 is the stream one bit further on (the parity position skipped)
-            *mp = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+            *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
           }
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
+        #pragma unroll 1
         for (uint32_t e = lane; e < np * T.rem; e += 32) {
           uint32_t c;
           const uint32_t p = divmod_small(e, T.rem, T.mag_rem, c);
@@ -613,23 +620,32 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];
           const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          mbuf[p * Wp + W] = ((__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z)) & d.w;
+          mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
         }
       }
     }
     __syncwarp();
-    if (npc > 0) {  // pass H: head words, one piece per lane, OR-ed in
-      for (uint32_t e = lane; e < np * npc; e += 32) {
+    if (nsp > 0) {  // pass H: head words (segment boundaries; without pass X also segment heads), one lane per word
+#pragma unroll 1
+      for (uint32_t e = lane; e < np * nsp; e += 32) {
         uint32_t c;
-        const uint32_t p = divmod_small(e, npc, T.mag_np, c);
-        const uint2 pc = pieces[c];
-        const uint32_t s0 = kPadBits + p * stride_bits + (pc.x & 0xFFFFu), len = (pc.x >> 16) & 63u;
-        const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
-        atomicOr(&mbuf[p * Wp + pc.y], x << ((pc.x >> 24) & 31u));
+        const uint32_t p = divmod_small(e, nsp, T.mag_ns, c);
+        const uint2 sp = spec[c];
+        const uint32_t pb = kPadBits + p * stride_bits;
+        uint32_t v = 0;
+#pragma unroll 1
+        for (uint32_t i = sp.y & 0xFFFFu; i < (sp.y >> 16); ++i) {
+          const uint32_t pc = pieces[i].x;
+          const uint32_t s0 = pb + (pc & 0xFFFFu), len = (pc >> 16) & 63u;
+          const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
+          v |= x << ((pc >> 24) & 31u);
+        }
+        mbuf[p * Wp + sp.x] = v;  // after pass R's store of this word
       }
     }
     __syncwarp();
     // per item: syndrome out, packet status, counts; a correctable error flips its data bit
+    #pragma unroll 1
     for (uint32_t i = lane; i < np * g.t; i += 32) {
       uint32_t seg;
       const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
@@ -674,8 +690,10 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * Wp * 4 + i];
       }
     }
-    if (a.status != nullptr)
-      for (uint32_t i = lane; i < np; i += 32) a.status[p0 + i] = static_cast<uint8_t>(pst[i]);
+    if (a.status != nullptr) {
+      if (static_cast<uint32_t>(lane) < np) a.status[p0 + lane] = static_cast<uint8_t>(pst[lane]);
+      if (static_cast<uint32_t>(lane) + 32 < np) a.status[p0 + lane + 32] = static_cast<uint8_t>(pst[lane + 32]);
+    }
     __syncwarp();
   }
   if (lane == 0) bulk_wait<0>();  // the last bulk stores have completed before shared memory goes away
