@@ -512,7 +512,6 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   }
   uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
   uint32_t* pst = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + kPktMsgBufs * bg.msg_cap);  // statuses
-  uint32_t* sbuf = pst + bg.G;  // per-item syndromes of the batch
   uint64_t* bars = bars_all + warp * kPktStages;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
@@ -555,8 +554,13 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     if (static_cast<uint32_t>(lane) + 32 < np) pst[lane + 32] = 0;
     mbar_wait(&bars[buf], (it / kPktStages) & 1u);
     __syncwarp();
-    {  // pass S: syndromes per (packet, segment) item, by groups of L lanes (reads the stream as received)
+    {  // pass S: per (packet, segment) item, by groups of L lanes: the checksum vector of the
+       // stream as received, then the item's epilogue -- syndrome out, packet status (max), counts, the
+       // correction as a flip of the stream bit at position s (ED/EC) -- and, with HX, pass X:
+       // the item's head compacted in place (the m = 6 RR of positions 0..63) for passes R and H
+      uint32_t* wm = const_cast<uint32_t*>(w);
       const uint32_t items = np * g.t;
+#pragma unroll 1
       for (uint32_t base = 0; base < items; base += groups) {
         const bool active = base + gid < items;
         uint32_t seg;
@@ -564,31 +568,44 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
         const uint32_t off = pk * stride_bits + sg[seg];
         const uint32_t s = group_syndrome64<L>(w, off, n, active, q);
-        if (active && q == 0) sbuf[base + gid] = s;
-      }
-    }
-    if constexpr (HX) {  // pass X: compact each segment's head in place (RR of positions 0..63)
-      __syncwarp();
-      uint32_t* wm = const_cast<uint32_t*>(w);
-      #pragma unroll 1
-      for (uint32_t i = lane; i < np * g.t; i += 32) {
-        uint32_t seg;
-        const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
-        const uint32_t o = pk * stride_bits + sg[seg] + kPadBits - 1;  // buffer bit of position 0
-        uint32_t* wq = wm + (o >> 5);
-        const uint32_t r = o & 31u;
-        const uint32_t w0 = wq[0], w1 = wq[1], w2 = wq[2];
-        const uint64_t x = static_cast<uint64_t>(__funnelshift_r(w0, w1, r)) |
-                           (static_cast<uint64_t>(__funnelshift_r(w1, w2, r)) << 32);  // bit p = position p
-        // data positions 3, 5..7, 9..15, 17..31, 33..63 -> bits 0..56 (the m = 6 compaction, App. A)
-        const uint64_t d = ((x >> 3) & 0x1ull) | ((x >> 4) & 0xeull) | ((x >> 5) & 0x7f0ull) |
-                           ((x >> 6) & 0x3fff800ull) | ((x >> 7) & 0x1fffffffc000000ull);
-        const uint64_t xn = (x & 0x7full) | (d << 7);  // positions 0..6 kept, data at 7..63
-        const uint32_t lo = static_cast<uint32_t>(xn), hi = static_cast<uint32_t>(xn >> 32);
-        const uint32_t lm = (1u << r) - 1u;
-        wq[0] = (w0 & lm) | (lo << r);
-        wq[1] = __funnelshift_l(lo, hi, r);
-        wq[2] = (w2 & ~lm) | __funnelshift_l(hi, 0u, r);
+        // every lane's loads of this round are done (the group reduction above is warp-synchronous):
+        // flipping a bit of this item cannot race with another item's reads, whose chunks never
+        // count a bit outside their own positions 0..n
+        const bool lead = active && q == 0;
+        if (lead) {
+          const bool corr = s != 0 && s <= n;
+          const bool fail = s > n;
+          if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
+          if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
+          n_corr += corr;
+          n_fail += fail;
+          if (corr) {  // position s is buffer bit kPadBits + off + s - 1
+            const uint32_t fb = kPadBits + off + s - 1;
+            atomicXor(&wm[fb >> 5], 1u << (fb & 31u));
+          }
+        }
+        if constexpr (HX) {
+          __syncwarp();  // every flip of this round has landed before a head word is rewritten
+          if (lead) {
+            const uint32_t o = off + kPadBits - 1;  // buffer bit of position 0
+            uint32_t* wq = wm + (o >> 5);
+            const uint32_t r = o & 31u;
+            const uint32_t w0 = wq[0], w1 = wq[1], w2 = wq[2];
+            const uint64_t x = static_cast<uint64_t>(__funnelshift_r(w0, w1, r)) |
+                               (static_cast<uint64_t>(__funnelshift_r(w1, w2, r)) << 32);  // bit p = position p
+            // data positions 3, 5..7, 9..15, 17..31, 33..63 -> bits 0..56 (the m = 6 compaction, App. A)
+            const uint64_t d = ((x >> 3) & 0x1ull) | ((x >> 4) & 0xeull) | ((x >> 5) & 0x7f0ull) |
+                               ((x >> 6) & 0x3fff800ull) | ((x >> 7) & 0x1fffffffc000000ull);
+            const uint64_t xn = (x & 0x7full) | (d << 7);  // positions 0..6 kept, data at 7..63
+            const uint32_t lo = static_cast<uint32_t>(xn), hi = static_cast<uint32_t>(xn >> 32);
+            const uint32_t lm = (1u << r) - 1u;
+            // plain read-modify-write: with k >= 96 no other item's head window or flip shares these
+            // words in this round, and the bits outside positions 7..63 are written back unchanged
+            wq[0] = (w0 & lm) | (lo << r);
+            wq[1] = __funnelshift_l(lo, hi, r);
+            wq[2] = (w2 & ~lm) | __funnelshift_l(hi, 0u, r);
+          }
+        }
       }
     }
     __syncwarp();
@@ -641,24 +658,6 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           v |= x << ((pc >> 24) & 31u);
         }
         mbuf[p * Wp + sp.x] = v;  // after pass R's store of this word
-      }
-    }
-    __syncwarp();
-    // per item: syndrome out, packet status, counts; a correctable error flips its data bit
-    #pragma unroll 1
-    for (uint32_t i = lane; i < np * g.t; i += 32) {
-      uint32_t seg;
-      const uint32_t pk = divmod_small(i, g.t, T.mag_t, seg);
-      const uint32_t s = sbuf[i], n = sg[kPktMaxSeg + seg];
-      const bool corr = s != 0 && s <= n;
-      const bool fail = s > n;
-      if (a.syn != nullptr) a.syn[p0 * g.t + i] = static_cast<uint16_t>(s);
-      if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
-      n_corr += corr;
-      n_fail += fail;
-      if (corr && (s & (s - 1)) != 0) {  // a data position: message bit moff + s - floor(log2 s) - 2
-        const uint32_t fb = sg[3 * kPktMaxSeg + seg] + s - (31u - __clz(s)) - 2;
-        atomicXor(&mbuf[pk * Wp + (fb >> 5)], 1u << (fb & 31u));
       }
     }
     __syncwarp();
