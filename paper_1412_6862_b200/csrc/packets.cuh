@@ -363,6 +363,7 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
 }
 
 struct BatchGeom {
+  uint32_t warps;      // warps per CTA (<= kPktWarps)
   uint32_t G;          // packets per batch
   uint32_t L;          // lanes per item in pass S (power of two)
   uint32_t in_cap;     // bytes per input buffer: 16 pad + G*stride + 16 slack
@@ -374,13 +375,26 @@ struct BatchGeom {
 hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
-#ifndef HAM_PKT_BUDGET
-#define HAM_PKT_BUDGET (6 * 1024)
-#endif
-  const uint64_t budget = HAM_PKT_BUDGET;  // shared bytes per warp (tuned: tools/tune_shapes.py packets)
+  // Launch shape (tools/tune_shapes.py packets): 16 warps per CTA with 6 KB of shared memory each
+  // (2 CTAs = 32 warps per SM), unless 8 warps with 13 KB each (still 16 warps per SM) fit at
+  // least 3 packets per batch -- then the per-batch costs (TMA issue, bulk store, status, loop
+  // set-up) are amortised over 3+ packets and the bytes in flight per SM grow, which measured
+  // better (M = 400..1200) than twice the warps with 1..2 packets per batch (M >= 1600).
   const uint64_t per = kPktStages * stride + kPktMsgBufs * 4ull * T.Wp + 4 + 4ull * g.t;
-  uint64_t G = budget > 96 ? (budget - 96) / per : 1;
-  G = std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
+  auto fit = [&](uint64_t budget) {
+    const uint64_t G = budget > 96 ? (budget - 96) / per : 1;
+    return std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
+  };
+  uint64_t G = fit(13312);
+  b.warps = 8;
+  if (G < 3) {
+    G = fit(6144);
+    b.warps = 16;
+  }
+#ifdef HAM_PKT_BUDGET
+  G = fit(HAM_PKT_BUDGET);
+  b.warps = kPktWarps;
+#endif
   b.G = static_cast<uint32_t>(G);
   // lanes per item in pass S: the L minimising an issue-count model of the pass --
   // ceil(items / (32 / L)) rounds, each a fixed set-up + epilogue (~90 warp
@@ -517,7 +531,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   __syncthreads();
   const uint64_t n_batches = (a.n_packets + bg.G - 1) / bg.G;
   const uint64_t gw = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x;  // CTA-minor (see tiles_kernel)
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPktWarps;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint64_t pol = policy_evict_first();
   const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
   const uint32_t groups = 32 / L;
@@ -727,7 +741,7 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const size_t smem = bg.tab_bytes + static_cast<size_t>(kPktWarps) * bg.warp_bytes;
+  const size_t smem = bg.tab_bytes + static_cast<size_t>(bg.warps) * bg.warp_bytes;
   if (smem > 227 * 1024) return set_err(HAMMING_E_ARG, "packets: shared memory budget exceeded");
   void (*kfn)(PacketGeom, BatchGeom, PacketArgs, PacketTables) = nullptr;
 #define HAM_PKT_KFN(HX)                                   \
@@ -751,13 +765,13 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kPktWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, bg.warps * 32, smem);
   if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets decode)");
   const uint64_t batches = (a.n_packets + bg.G - 1) / bg.G;
-  const uint64_t want = (batches + kPktWarps - 1) / kPktWarps;
+  const uint64_t want = (batches + bg.warps - 1) / bg.warps;
   const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
   if (grid > 0) {
-    kfn<<<grid, kPktWarps * 32, smem, st>>>(g, bg, a, T);
+    kfn<<<grid, bg.warps * 32, smem, st>>>(g, bg, a, T);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "packets decode launch");
   }
