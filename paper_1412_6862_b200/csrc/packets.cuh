@@ -287,6 +287,10 @@ struct PacketTables {
   uint32_t special[kPktMaxSpecial + 1];  // word index | first piece << 16; [n_special]: end
   uint32_t piece[kPktMaxPieces];         // src (bits 0..15) | len (16..21) | pos (24..28)
   uint16_t piece_word[kPktMaxPieces];    // the head word a piece belongs to
+  // with headx, the word straddling the start of segment i (i >= 1) is assembled by pass X:
+  // bw[i] = its word index (0xFFFFFFFF: segment i starts word-aligned), bsrc[i] = src | nb0 << 16
+  // of the last blen[i] data bits of segment i-1 (two slices, as in pass R), which fill its low bits
+  uint32_t bw[kPktMaxSeg], bsrc[kPktMaxSeg], blen[kPktMaxSeg];
 };
 // src = bit of the packet stream (from its first bit) holding the slice's first data bit.
 
@@ -342,7 +346,7 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
     } else {
       if (T.n_special >= kPktMaxSpecial || T.n_pieces + np > kPktMaxPieces)
         return set_err(HAMMING_E_ARG, "packets: piece table overflow");
-      T.word0[W] = 33u << 16;  // head word: pass H overwrites what pass R stored
+      T.word0[W] = 33u << 16;  // head word: not written by pass R
       T.special[T.n_special++] = W | (T.n_pieces << 16);
       for (uint32_t i = 0; i < np; ++i) {
         T.piece_word[T.n_pieces] = static_cast<uint16_t>(W);
@@ -351,6 +355,34 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
     }
   }
   T.special[T.n_special] = T.n_pieces << 16;
+  for (uint32_t i = 0; i < kPktMaxSeg; ++i) T.bw[i] = 0xFFFFFFFFu, T.bsrc[i] = 0, T.blen[i] = 0;
+  if (T.headx) {  // every head word must be one segment boundary: <= 2 tail slices, then the head
+    for (uint32_t e = 0; e < T.n_special; ++e) {
+      const uint32_t W = T.special[e] & 0xFFFFu, p0 = T.special[e] >> 16, p1 = T.special[e + 1] >> 16;
+      uint32_t lt = 0, nt = 0, src0 = 0, len0 = 0;
+      bool ok = p1 > p0;
+      for (uint32_t q = p0; ok && q < p1; ++q) {
+        const uint32_t src = T.piece[q] & 0xFFFFu, len = (T.piece[q] >> 16) & 63u, pos = T.piece[q] >> 24;
+        if (q + 1 < p1) {  // a tail slice of segment i - 1
+          if (nt == 0) src0 = src, len0 = len;
+          else ok = ok && nt == 1 && src == src0 + len0 + 1;
+          ok = ok && pos == lt;
+          lt += len;
+          ++nt;
+        } else {  // the head of segment i: data index 0 at position 7
+          uint32_t i = 1;
+          while (i < g.t && g.moff[i] != 32u * W + lt) ++i;
+          ok = ok && nt >= 1 && i < g.t && pos == lt && len == 32u - lt && src == g.off[i] + 6;
+          if (ok) {
+            T.bw[i] = W;
+            T.bsrc[i] = src0 | ((nt == 1 ? 32u : len0) << 16);
+            T.blen[i] = lt;
+          }
+        }
+      }
+      if (!ok) return set_err(HAMMING_E_ARG, "packets: unexpected head word layout");
+    }
+  }
   auto mag = [](uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : static_cast<uint32_t>((1ull << 32) / d); };
   T.mag_t = mag(g.t);
   T.mag_ns = mag(T.n_special);
@@ -417,7 +449,7 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
   b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
                  static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
-  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 4 * kPktMaxSeg + 15) / 16 * 16;
+  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
   if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
     return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
   return HAMMING_OK;
@@ -503,7 +535,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   __shared__ unsigned long long cta_counts[2];
   __shared__ __align__(8) uint64_t bars_all[kPktWarps * kPktStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t Wp = T.Wp, nsp = T.n_special;
+  const uint32_t Wp = T.Wp, nsp = HX ? 0u : T.n_special;  // with HX pass X writes the head words
   // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
   // pieces {src | len | pos, word}, per-segment geometry
   uint4* wdesc = reinterpret_cast<uint4*>(smem);
@@ -512,7 +544,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   uint32_t* sg = reinterpret_cast<uint32_t*>(spec + T.n_special);  // [off | n | k | moff] x kPktMaxSeg
   for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
-    const bool head = nb > 32;  // head words: pass H overwrites them
+    const bool head = nb > 32;  // head words: pass R skips them (pass H, or with HX pass X, writes them)
     wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, head ? 0u : 0xFFFFFFFFu);
   }
   for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = make_uint2(T.piece[i], T.piece_word[i]);
@@ -523,6 +555,9 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     sg[kPktMaxSeg + threadIdx.x] = g.n[threadIdx.x];
     sg[2 * kPktMaxSeg + threadIdx.x] = g.k[threadIdx.x];
     sg[3 * kPktMaxSeg + threadIdx.x] = g.moff[threadIdx.x];
+    sg[4 * kPktMaxSeg + threadIdx.x] = T.bw[threadIdx.x];
+    sg[5 * kPktMaxSeg + threadIdx.x] = T.bsrc[threadIdx.x];
+    sg[6 * kPktMaxSeg + threadIdx.x] = T.blen[threadIdx.x];
   }
   uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
   uint32_t* pst = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + kPktMsgBufs * bg.msg_cap);  // statuses
@@ -618,6 +653,17 @@ __global__ void __launch_bounds__(kPktWarps * 32)
             wq[0] = (w0 & lm) | (lo << r);
             wq[1] = __funnelshift_l(lo, hi, r);
             wq[2] = (w2 & ~lm) | __funnelshift_l(hi, 0u, r);
+            const uint32_t W = sg[4 * kPktMaxSeg + seg];
+            if (W != 0xFFFFFFFFu) {  // the message word straddling this segment's start (pass R skips it):
+              // the last lt data bits of segment seg - 1 (corrected: its round came first), then the head
+              const uint32_t bs = sg[5 * kPktMaxSeg + seg], lt = sg[6 * kPktMaxSeg + seg];
+              const uint32_t s0 = kPadBits + pk * stride_bits + (bs & 0xFFFFu), nb0 = bs >> 16;
+              const uint32_t a0 = wm[s0 >> 5], a1 = wm[(s0 >> 5) + 1];
+              const uint32_t m0 = __funnelshift_lc(0xFFFFFFFFu, 0u, nb0);
+              const uint32_t tail = ((__funnelshift_r(a0, a1, s0) & m0) | (__funnelshift_rc(a0, a1, (s0 & 31u) + 1) & ~m0)) &
+                                    __funnelshift_lc(0xFFFFFFFFu, 0u, lt);
+              mbuf[pk * Wp + W] = tail | (static_cast<uint32_t>(d) << lt);
+            }
           }
         }
       }
@@ -629,17 +675,17 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         for (uint32_t W = lane; W < Wp; W += 32) {
           const uint4 d = wdesc[W];
           const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
-          mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+          if (d.w) mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
         }
       } else {
         for (uint32_t W = lane; W < T.Wfull; W += 32) {
-          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, -}
+          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
           uint32_t* mp = mbuf + W;
           for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
             const uint32_t a0 = wp[0], a1 = wp[1];
             // slice 1 is the stream one bit further on (the parity position skipped)
-            *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+            if (d.w) *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
           }
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
@@ -651,7 +697,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];
           const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+          if (d.w) mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
         }
       }
     }
@@ -671,7 +717,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint32_t x = __funnelshift_r(w[s0 >> 5], w[(s0 >> 5) + 1], s0) & __funnelshift_lc(0xFFFFFFFFu, 0u, len);
           v |= x << ((pc >> 24) & 31u);
         }
-        mbuf[p * Wp + sp.x] = v;  // after pass R's store of this word
+        mbuf[p * Wp + sp.x] = v;
       }
     }
     __syncwarp();
