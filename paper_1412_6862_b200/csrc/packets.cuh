@@ -443,6 +443,9 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
 #ifdef HAM_PKT_L
   L = HAM_PKT_L;
 #endif
+#ifdef HAM_PKT_TUNE  // tuning builds only: lanes per item from the environment
+  if (const char* e = getenv("HAM_PKT_L")) L = static_cast<uint32_t>(atoi(e));
+#endif
   b.L = L;
   b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
   b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
