@@ -407,19 +407,26 @@ struct BatchGeom {
 hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
-  // Launch shape (tools/tune_shapes.py packets): 16 warps per CTA with 6 KB of shared memory each
-  // (2 CTAs = 32 warps per SM), unless 8 warps with 13 KB each (still 16 warps per SM) fit at
-  // least 3 packets per batch -- then the per-batch costs (TMA issue, bulk store, status, loop
-  // set-up) are amortised over 3+ packets and the bytes in flight per SM grow, which measured
-  // better (M = 400..1200) than twice the warps with 1..2 packets per batch (M >= 1600).
+  // Launch shape, measured (tools/tune_shapes.py packets): the trade is warps per SM
+  // (latency hiding) against packets per batch (the per-batch costs -- TMA issue, bulk store,
+  // status, loop set-up -- amortised, and more bytes in flight per warp).  In order:
+  //   >= 6 packets with 12 warps x 9 KB (2 CTAs = 24 warps/SM)   M ~ 400
+  //   >= 4 packets with  8 warps x 13 KB (16 warps/SM)            M ~ 800
+  //   >= 2 packets with 12 warps x 9 KB                           M ~ 1200
+  //   else 16 warps x 6 KB (32 warps/SM, usually 1 packet)        M >= 1600
   const uint64_t per = kPktStages * stride + kPktMsgBufs * 4ull * T.Wp + 4 + 4ull * g.t;
   auto fit = [&](uint64_t budget) {
     const uint64_t G = budget > 96 ? (budget - 96) / per : 1;
     return std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
   };
-  uint64_t G = fit(13312);
-  b.warps = 8;
-  if (G < 3) {
+  uint64_t G;
+  if ((G = fit(9216)) >= 6) {
+    b.warps = 12;
+  } else if ((G = fit(13312)) >= 4) {
+    b.warps = 8;
+  } else if ((G = fit(9216)) >= 2) {
+    b.warps = 12;
+  } else {
     G = fit(6144);
     b.warps = 16;
   }
@@ -427,19 +434,35 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   G = fit(HAM_PKT_BUDGET);
   b.warps = kPktWarps;
 #endif
-  b.G = static_cast<uint32_t>(G);
   // lanes per item in pass S: the L minimising an issue-count model of the pass --
   // ceil(items / (32 / L)) rounds, each a fixed set-up + epilogue (~90 warp
   // instructions, + 4 per shuffle step) and ceil(C64 / 4L) unrolled blocks of
-  // ~42 -- so short codewords and many items per batch take small groups
-  const uint32_t items = static_cast<uint32_t>(G) * g.t, c64 = (maxn + 1) / 64 + 1;
+  // ~42 -- so short codewords and many items per batch take small groups.  The
+  // batch may also shrink (down to half the shape's G) when fewer packets fill
+  // the rounds better: the model's cost per packet counts ~150 more per batch.
+  const uint32_t c64 = (maxn + 1) / 64 + 1;
+  auto best_L = [&](uint64_t Gc, uint32_t& L) {
+    const uint32_t items = static_cast<uint32_t>(Gc) * g.t;
+    uint64_t best = ~0ull;
+    for (uint32_t l = 1, lg = 0; l <= 32; l *= 2, ++lg) {
+      const uint64_t rounds = (items + 32 / l - 1) / (32 / l);
+      const uint64_t cost = rounds * (90 + 4 * (l == 32 ? 0 : lg) + 42 * ((c64 + 4 * l - 1) / (4 * l)));
+      if (cost < best) best = cost, L = l;
+    }
+    return best;
+  };
   uint32_t L = 1;
-  uint64_t best = ~0ull;
-  for (uint32_t l = 1, lg = 0; l <= 32; l *= 2, ++lg) {
-    const uint64_t rounds = (items + 32 / l - 1) / (32 / l);
-    const uint64_t cost = rounds * (90 + 4 * (l == 32 ? 0 : lg) + 42 * ((c64 + 4 * l - 1) / (4 * l)));
-    if (cost < best) best = cost, L = l;
+  {
+    uint64_t Gbest = G;
+    double score = 1e300;
+    for (uint64_t Gc = G; Gc >= 1 && 2 * Gc >= G; --Gc) {
+      uint32_t l = 1;
+      const double sc = static_cast<double>(best_L(Gc, l) + 150) / static_cast<double>(Gc);
+      if (sc < score * 0.999) score = sc, Gbest = Gc, L = l;
+    }
+    G = Gbest;
   }
+  b.G = static_cast<uint32_t>(G);
 #ifdef HAM_PKT_L
   L = HAM_PKT_L;
 #endif

@@ -32,7 +32,7 @@ SECDED_VARIANTS = {
     5: [(12, 3), (8, 4), (16, 2), (8, 3)],
     6: [(8, 3), (12, 2), (8, 2)],
 }
-PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((6144, 2, 1, 16), (8192, 2, 1, 16), (10240, 2, 1, 16), (8192, 2, 1, 12), (12288, 2, 1, 8), (13312, 2, 1, 8), (16384, 2, 1, 8), (9216, 3, 1, 8), (12288, 3, 1, 8))]
+PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((6144, 2, 1, 16), (13312, 2, 1, 8), (9216, 2, 1, 8), (7168, 2, 1, 8), (9216, 2, 1, 12), (6656, 2, 1, 12))]
 
 
 def name(m, v):
@@ -86,7 +86,7 @@ def run():
         for b, st, mb, w in PKT_VARIANTS:
             env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"))
             print("budget", b, "stages", st, "msgbufs", mb, "warps", w, flush=True)
-            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "1200", "1600",
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "800", "1200", "1600",
                             "2000", "--t", "2", "3", "6"], env=env)
         return
     for m, vs in VARIANTS.items():
