@@ -667,6 +667,13 @@ __device__ __forceinline__ void load_swizzled(const uint32_t* __restrict__ tile,
 __device__ __forceinline__ uint32_t secded_flags(uint32_t s, uint32_t par) {
   return s | (par << 6) | ((static_cast<uint32_t>(s != 0) & (par ^ 1u)) << 7);
 }
+// the same for four codewords at once: S4 holds s_k in byte k (s_k < 64), P4 holds P_k at bit
+// 8k + 6; byte k of the result is secded_flags(s_k, P_k) (s_k + 0x7F carries into bit 7 iff
+// s_k != 0, never out of the byte)
+__device__ __forceinline__ uint32_t secded_flags4(uint32_t S4, uint32_t P4) {
+  const uint32_t nz = (S4 + 0x7F7F7F7Fu) & 0x80808080u;
+  return S4 | P4 | (nz & ~(P4 << 1));
+}
 
 // (8,4): a codeword is one byte; per-lane replicated 256-entry table of 8-byte
 // entries {final data nibble replicated into all eight nibbles, flags} (64 KB),
@@ -766,6 +773,7 @@ struct DecodeSecded4Op {
     uint32_t o[11];
 #pragma unroll
     for (int i = 0; i < 11; ++i) o[i] = 0;
+    uint32_t S4 = 0, P4 = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const uint32_t cw = (w[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
@@ -776,7 +784,12 @@ struct DecodeSecded4Op {
       const int b = 11 * c, q = b >> 5, r = b & 31;
       o[q] |= d << r;
       if (r > 21) o[q + 1] |= d >> (32 - r);
-      side[c >> 2] |= secded_flags(s, par) << (8 * (c & 3));
+      S4 |= s << (8 * (c & 3));
+      P4 |= par << (8 * (c & 3) + 6);
+      if ((c & 3) == 3) {
+        side[c >> 2] |= secded_flags4(S4, P4);
+        S4 = P4 = 0;
+      }
     }
 #pragma unroll
     for (int i = 0; i < 11; ++i) out[i] = o[i];
@@ -810,6 +823,7 @@ struct DecodeSecded5Op {
     uint32_t o[26];
 #pragma unroll
     for (int i = 0; i < 26; ++i) o[i] = 0;
+    uint32_t S4 = 0, P4 = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       const uint32_t x = w[c];
@@ -822,7 +836,12 @@ struct DecodeSecded5Op {
       const uint32_t f = *reinterpret_cast<const uint32_t*>(sh + 65536 + (s << 7) + lane4);
       const uint32_t d = ((elo & 0x7FFu) | ((h << 10) & 0x3FFF800u)) ^ (par ? f : 0u);
       put_bits(o, 26 * c, d, 26);
-      side[c >> 2] |= secded_flags(s, par) << (8 * (c & 3));
+      S4 |= s << (8 * (c & 3));
+      P4 |= par << (8 * (c & 3) + 6);
+      if ((c & 3) == 3) {
+        side[c >> 2] |= secded_flags4(S4, P4);
+        S4 = P4 = 0;
+      }
     }
 #pragma unroll
     for (int i = 0; i < 26; ++i) out[i] = o[i];
