@@ -342,6 +342,18 @@ __host__ __device__ __forceinline__ constexpr uint32_t swz_unit(uint32_t g) {
   return r * 8 + ((g ^ r) & 7u);
 }
 
+// flags byte of a SECDED codeword from its syndrome and overall parity
+__device__ __forceinline__ uint32_t secded_flags(uint32_t s, uint32_t par) {
+  return s | (par << 6) | ((static_cast<uint32_t>(s != 0) & (par ^ 1u)) << 7);
+}
+// the same for four codewords at once: S4 holds s_k in byte k (s_k < 64), P4 holds P_k at bit
+// 8k + 6; byte k of the result is secded_flags(s_k, P_k) (s_k + 0x7F carries into bit 7 iff
+// s_k != 0, never out of the byte)
+__device__ __forceinline__ uint32_t secded_flags4(uint32_t S4, uint32_t P4) {
+  const uint32_t nz = (S4 + 0x7F7F7F7Fu) & 0x80808080u;
+  return S4 | P4 | (nz & ~(P4 << 1));
+}
+
 template <int M, bool EXT = false>
 struct DecodeOp {
   static constexpr int CW_BITS = EXT ? (1 << M) : Geo<M>::n;
@@ -405,6 +417,7 @@ struct DecodeOp {
     uint32_t o[k];
 #pragma unroll
     for (int i = 0; i < k; ++i) o[i] = 0;
+    uint32_t S4 = 0, P4 = 0;
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       uint32_t lo, hi = 0;
@@ -423,9 +436,8 @@ struct DecodeOp {
         if constexpr (M == 6) hi = take_bits(w, c * n + 31);
       }
       const uint32_t s = syndrome_cw<M>(lo, hi);  // a2
-      uint32_t flag = 0;
+      uint32_t par = 0;
       if constexpr (EXT) {  // overall parity P decides: P = 1 correct, P = 0 and s != 0 detect
-        uint32_t par;
         if constexpr (M == 6) par = __popc(lo ^ hi) & 1u;
         else if constexpr (M == 5) par = __popc(lo) & 1u;
         else par = __popc(lo & ((1u << CW_BITS) - 1u)) & 1u;
@@ -436,8 +448,6 @@ struct DecodeOp {
           lo ^= static_cast<uint32_t>(f);
           hi ^= static_cast<uint32_t>(f >> 32);
         }
-        const uint32_t ded = ((s + 63u) >> 6) & (par ^ 1u);  // s != 0 (s <= 63) and P = 0
-        flag = (par << 6) | (ded << 7);
       } else if constexpr (M <= 5) {  // a3 (s = 0 flips the dummy bit 0)
         lo ^= 1u << s;
       } else {
@@ -451,7 +461,16 @@ struct DecodeOp {
       for (int g = 1; g < (M <= 5 ? M : 5); ++g)
         put_field(o, c * k + (1 << g) - g - 1, lo, (1 << g) + 1, (1 << g) - 1);
       if constexpr (M == 6) put_field(o, c * k + 26, hi, 1, 31);
-      side[c >> 2] |= (s | flag) << (8 * (c & 3));
+      if constexpr (EXT) {  // flags bytes {s, P << 6, (s != 0 and P = 0) << 7}, four at a time
+        S4 |= s << (8 * (c & 3));
+        P4 |= par << (8 * (c & 3) + 6);
+        if ((c & 3) == 3) {
+          side[c >> 2] |= secded_flags4(S4, P4);
+          S4 = P4 = 0;
+        }
+      } else {
+        side[c >> 2] |= s << (8 * (c & 3));
+      }
     }
 #pragma unroll
     for (int i = 0; i < k; ++i) out[i] = o[i];
@@ -663,17 +682,6 @@ __device__ __forceinline__ void load_swizzled(const uint32_t* __restrict__ tile,
   }
 }
 
-// flags byte of a SECDED codeword from its syndrome and overall parity
-__device__ __forceinline__ uint32_t secded_flags(uint32_t s, uint32_t par) {
-  return s | (par << 6) | ((static_cast<uint32_t>(s != 0) & (par ^ 1u)) << 7);
-}
-// the same for four codewords at once: S4 holds s_k in byte k (s_k < 64), P4 holds P_k at bit
-// 8k + 6; byte k of the result is secded_flags(s_k, P_k) (s_k + 0x7F carries into bit 7 iff
-// s_k != 0, never out of the byte)
-__device__ __forceinline__ uint32_t secded_flags4(uint32_t S4, uint32_t P4) {
-  const uint32_t nz = (S4 + 0x7F7F7F7Fu) & 0x80808080u;
-  return S4 | P4 | (nz & ~(P4 << 1));
-}
 
 // (8,4): a codeword is one byte; per-lane replicated 256-entry table of 8-byte
 // entries {final data nibble replicated into all eight nibbles, flags} (64 KB),
