@@ -1226,6 +1226,19 @@ struct TileLayout {
   }
 };
 
+#ifdef HAM_TIMING  // debug builds only: per-CTA %globaltimer stamps (tools/timing_probe.py)
+__device__ unsigned long long g_timing[1024 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HAM_STAMP(i) \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_timing[blockIdx.x * 4 + (i)] = gtimer()
+#else
+#define HAM_STAMP(i)
+#endif
+
 template <class Op, int WARPS, int STAGES, bool INPLACE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
@@ -1238,6 +1251,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long block_cnt[2];
 
+  HAM_STAMP(0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* const sh = smem;  // Op::SHARED bytes of CTA-wide tables first
   // 128-byte-swizzled TMA destinations must be 1024-byte aligned
@@ -1280,6 +1294,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     uint32_t* obuf;
     if constexpr (TL::IN_PLACE) {
       mbar_wait(&bars[st], (it / STAGES) & 1u);
+#ifdef HAM_TIMING
+      if (it == 0) HAM_STAMP(1);
+#endif
       obuf = reinterpret_cast<uint32_t*>(wbase + st * IN);
     } else {
       if constexpr (IN > 0) mbar_wait(&bars[st], (it / STAGES) & 1u);
@@ -1335,7 +1352,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     cnt += run_tail_tile<Op>(in, out, side, n_full, rem, in_total, out_total, wbase,
                              reinterpret_cast<uint32_t*>(tail_out), lane, args, sh, cnt2);
   }
+  HAM_STAMP(2);
   if (lane == 0) bulk_wait<0>();
+  HAM_STAMP(3);
 
   if (counter != nullptr) {
     cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -1399,6 +1418,10 @@ struct Launcher {
     if (dev < 0 || dev >= kMaxDev || !configured[dev].load(std::memory_order_acquire)) {
       e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
       if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+#ifdef HAM_CARVEOUT
+      e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, HAM_CARVEOUT);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+#endif
       int occ = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, WARPS * 32, SMEM);
       if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
@@ -1664,6 +1687,11 @@ HostSlotLayout host_slot_layout(int m, uint64_t chunk, int with_syn) {
 extern "C" {
 
 int hamming_abi_version(void) { return HAMMING_ABI_VERSION; }
+#ifdef HAM_TIMING
+int hamming_debug_timing(unsigned long long* host_out, int n) {
+  return cudaMemcpyFromSymbol(host_out, g_timing, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 uint64_t hamming_coded_bytes(int m, uint64_t N) {
   if (m < 2 || m > 8 || bits_overflow(m, N)) return 0;
