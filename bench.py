@@ -239,8 +239,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # HAMMING_BENCH_BACKEND=gloo (testing only): run the N > 1 path with several ranks on
+        # however many GPUs the box has (ranks share a GPU), e.g. 2 ranks on a 1-GPU box
+        backend = os.environ.get("HAMMING_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
