@@ -998,6 +998,83 @@ struct EncodeLutOp {
   }
 };
 
+// m = 5 table encoder (perfect and SECDED): the codeword is linear in the 26
+// data bits, so it is the XOR of four table entries, one per data chunk (bits
+// 0..6, 7..13, 14..19, 20..25), each entry the whole codeword (stream form;
+// SECDED: with its overall-parity contribution in bit 0) of that chunk alone.
+// Per-lane replicated (entry e for lane l at word e * 32 + l: conflict free),
+// 384 entries = 48 KB, built at CTA start from encode_cw itself.  The POPC
+// encoder needs 5 (SECDED 6) POPCs per codeword and is XU-bound there.
+template <bool EXT>
+struct EncodeLut5Op {
+  static constexpr int CW_BITS = EXT ? 32 : 31;
+  static constexpr int k = 26;
+  static constexpr int IN_W = k, OUT_W = CW_BITS, IN_BITS = k;
+  static constexpr bool HAS_SIDE = false;
+  static constexpr int NCOUNT = 1;
+  static constexpr int ENTRIES = 128 + 128 + 64 + 64;
+  static constexpr int SHARED = ENTRIES * 32 * 4;
+  static constexpr bool SWZ_OUT = EXT;  // (32,26) tiles: the swizzled tensor-map store of EncodeOp<5, true>
+  struct NoArgs {};
+  struct OutArgs {
+    CUtensorMap tmap_out;
+  };
+  using Args = typename std::conditional<SWZ_OUT, OutArgs, NoArgs>::type;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&)[8]) { return 0; }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
+
+  __device__ __forceinline__ static uint32_t codeword(uint32_t d) {
+    uint32_t lo, hi;
+    encode_cw<5>(d, 0u, lo, hi);
+    if constexpr (EXT) return (lo & ~1u) | (static_cast<uint32_t>(__popc(lo & ~1u)) & 1u);
+    else return lo >> 1;
+  }
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    uint32_t* T = reinterpret_cast<uint32_t*>(sh);
+    for (int e = tid; e < ENTRIES * 32; e += nth) {
+      const uint32_t x = static_cast<uint32_t>(e >> 5);
+      const uint32_t d = x < 128 ? x : x < 256 ? (x - 128) << 7 : x < 320 ? (x - 256) << 14 : (x - 320) << 20;
+      T[e] = codeword(d);
+    }
+  }
+
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&)[8], uint64_t, int, const Args&, const uint8_t* sh) {
+    uint32_t w[k];
+#pragma unroll
+    for (int i = 0; i < k; ++i) w[i] = in[i];
+    const uint32_t lane4 = (threadIdx.x & 31u) << 2;
+    const uint8_t* t0 = sh + lane4;
+    const uint8_t* t1 = sh + (128u << 7) + lane4;
+    const uint8_t* t2 = sh + (256u << 7) + lane4;
+    const uint8_t* t3 = sh + (320u << 7) + lane4;
+    uint32_t o[OUT_W];
+#pragma unroll
+    for (int i = 0; i < OUT_W; ++i) o[i] = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t d = take_bits(w, c * k);
+      const uint32_t v = *reinterpret_cast<const uint32_t*>(t0 + ((d & 0x7Fu) << 7)) ^
+                         *reinterpret_cast<const uint32_t*>(t1 + (((d >> 7) & 0x7Fu) << 7)) ^
+                         *reinterpret_cast<const uint32_t*>(t2 + (((d >> 14) & 0x3Fu) << 7)) ^
+                         *reinterpret_cast<const uint32_t*>(t3 + (((d >> 20) & 0x3Fu) << 7));
+      if constexpr (EXT) o[c] = v;
+      else put_bits(o, c * CW_BITS, v, CW_BITS);
+    }
+    if constexpr (SWZ_OUT) {  // `out` is the output tile base
+      const uint32_t l = threadIdx.x & 31u;
+#pragma unroll
+      for (int u = 0; u < OUT_W / 4; ++u)
+        reinterpret_cast<uint4*>(out - l * OUT_W)[swz_unit<OUT_W>(l * (OUT_W / 4) + u)] =
+            make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < OUT_W; ++i) out[i] = o[i];
+    }
+  }
+};
+
 // splitmix64 output function (Steele, Lea & Flood 2014) -- written here
 // independently of oracle/oracle.c; the two are compared byte for byte.
 __device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {
@@ -1754,7 +1831,7 @@ hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_
 #define HAM_ENC_S4 4
 #endif
 #ifndef HAM_ENC_W5
-#define HAM_ENC_W5 12
+#define HAM_ENC_W5 8
 #define HAM_ENC_S5 3
 #endif
 #ifndef HAM_SENC_W3
@@ -1791,7 +1868,7 @@ hamming_status hamming_encode(int m, const void* data_dev, uint64_t N, void* rx_
     case 2: return Launcher<EncodeOp<2>, Shape<2>::W, Shape<2>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
     case 3: return Launcher<EncodeLutOp<3>, HAM_ENC_W3, HAM_ENC_S3>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
     case 4: return Launcher<EncodeLutOp<4>, HAM_ENC_W4, HAM_ENC_S4>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    case 5: return Launcher<EncodeOp<5>, HAM_ENC_W5, HAM_ENC_S5>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
+    case 5: return Launcher<EncodeLut5Op<false>, HAM_ENC_W5, HAM_ENC_S5>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
     case 6: return Launcher<EncodeOp<6>, Shape<6>::W, Shape<6>::S>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_encode: m must be in [2, 6]");
@@ -1981,7 +2058,7 @@ hamming_status hamming_encode_secded(int m, const void* data_dev, uint64_t N, vo
   switch (m) {
     case 3: return Launcher<EncodeLutOp<3, true>, HAM_SENC_W3, HAM_SENC_S3, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
     case 4: return Launcher<EncodeLutOp<4, true>, HAM_SENC_W4, HAM_SENC_S4, false>::run(in, out, nullptr, N, ib, ob, nullptr, {}, st);
-    case 5: return run_swizzled_out<EncodeOp<5, true>, HAM_SENC_W5, HAM_SENC_S5>(in, out, N, ib, ob, st);
+    case 5: return run_swizzled_out<EncodeLut5Op<true>, HAM_SENC_W5, HAM_SENC_S5>(in, out, N, ib, ob, st);
     case 6: return run_swizzled_out<EncodeOp<6, true>, HAM_SENC_W6, HAM_SENC_S6>(in, out, N, ib, ob, st);
   }
   return set_err(HAMMING_E_INVALID_M, "hamming_encode_secded: m must be in [3, 6]");
