@@ -1831,8 +1831,8 @@ hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_
 #define HAM_ENC_S4 4
 #endif
 #ifndef HAM_ENC_W5
-#define HAM_ENC_W5 8
-#define HAM_ENC_S5 3
+#define HAM_ENC_W5 10
+#define HAM_ENC_S5 2
 #endif
 #ifndef HAM_SENC_W3
 #define HAM_SENC_W3 16
@@ -1843,8 +1843,8 @@ hamming_status hamming_decode(int m, const void* rx_dev, uint64_t N, void* data_
 #define HAM_SENC_S4 3
 #endif
 #ifndef HAM_SENC_W5
-#define HAM_SENC_W5 8
-#define HAM_SENC_S5 3
+#define HAM_SENC_W5 4
+#define HAM_SENC_S5 8
 #endif
 #ifndef HAM_SENC_W6
 #define HAM_SENC_W6 6
