@@ -140,3 +140,29 @@ def test_random_geometries_strides_and_batches(oracle, M, t, extra):
     k, n = ham.packet_layout(M, t)
     n = np.array(n)
     assert cnt.tolist() == [int(((ws > 0) & (ws <= n)).sum()), int((ws > n).sum())]
+
+
+@pytest.mark.parametrize("M,t", [(400, 5), (800, 3), (1200, 6), (2000, 2), (97, 8), (11, 1)])
+def test_many_packets_multi_round(oracle, M, t):
+    """200k packets: every warp of the persistent grid walks many batches and
+    reuses its TMA stages and message buffer (the small tests stay in the first
+    round).  One error per segment (the paper's regime): every message must come
+    back as sent (the GPU generator is checked against the oracle above), the
+    counts must be [P t, 0] and every status 1; three windows of packets are
+    checked against the oracle byte for byte, syndromes included."""
+    P = 200_000
+    stride = ham.packet_stride(M, t)
+    rx, sent = ham.packet_channel_generate(M, t, 0x5EED, 0, P, p=1.0, want_messages=True)
+    res = ham.decode_packets(M, t, rx, P)
+    torch.cuda.synchronize()
+    msgs = res.messages.cpu().numpy()[: P * M]
+    assert np.array_equal(msgs, sent.cpu().numpy()[: P * M])
+    assert res.counts.cpu().numpy().tolist() == [P * t, 0]
+    assert (res.status.cpu().numpy()[:P] == 1).all()
+    rx_np = rx.cpu().numpy()
+    syn = res.syndromes.cpu().numpy().view(np.uint16)[: P * t].reshape(P, t)
+    for p0 in (0, P // 2 - 7, P - 300):
+        cnt = 300
+        wm, ws, wst = oracle.decode_packets(M, t, rx_np[p0 * stride:(p0 + cnt) * stride], cnt, stride)
+        assert np.array_equal(msgs[p0 * M:(p0 + cnt) * M], wm)
+        assert np.array_equal(syn[p0:p0 + cnt].reshape(-1), ws.reshape(-1))

@@ -199,3 +199,47 @@ def test_long_perfect_codes_random_streams(oracle, m):
     for N in (5, 128 * 37 + 11):
         rx = rng.integers(0, 256, ham.coded_bytes(m, N), dtype=np.uint8)
         assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+def _encoder_windows(N):
+    """Codeword windows (start, count) checked against the oracle in the large
+    encoder tests: starts are multiples of 8 so every window is byte-aligned
+    in both the data and the coded stream; the last one ends at N."""
+    last = (N - 4096) // 8 * 8
+    return [(0, 4096), (N // 2 // 8 * 8, 4096), (last, N - last)]
+
+
+@pytest.mark.parametrize("secded", [False, True])
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+def test_gpu_encoder_large_multi_round(oracle, m, secded):
+    """~6M codewords: every warp of the persistent grid walks many tiles and
+    wraps its TMA stage ring several times (the small encoder tests stay in the
+    first round), plus a ragged tail.  Oracle-checked on three byte-aligned
+    windows; the whole output round-trips through the (oracle-checked) GPU
+    decoder with zero syndromes."""
+    n, k = oracle.code_nk(m)
+    w = (n + 1) if secded else n
+    N = 6_000_003
+    rng = np.random.default_rng(100 + m + 10 * secded)
+    data = rng.integers(0, 256, ham.data_bytes(m, N), dtype=np.uint8)
+    enc = ham.encode_secded if secded else ham.encode
+    got = enc(m, gpu(data), N)
+    torch.cuda.synchronize()
+    out_bytes = (w * N + 7) // 8
+    got_np = got.cpu().numpy()[:out_bytes]
+    for c0, cnt in _encoder_windows(N):
+        d0, d1 = c0 * k // 8, (c0 * k + cnt * k + 7) // 8
+        want = (oracle.encode_secded if secded else oracle.encode)(m, np.ascontiguousarray(data[d0:d1]), cnt)
+        o0 = c0 * w // 8
+        assert np.array_equal(got_np[o0:o0 + want.size], want), (m, secded, c0)
+    if secded:
+        res = ham.decode_secded(m, got, N)
+        torch.cuda.synchronize()
+        assert int(res.counts.cpu().numpy().sum()) == 0
+    else:
+        res = ham.decode(m, got, N)
+        torch.cuda.synchronize()
+        assert int(res.corrected.item()) == 0
+    dec = res.data.cpu().numpy()[: ham.data_bytes(m, N)]
+    assert np.array_equal(np.unpackbits(dec, bitorder="little")[: N * k],
+                          np.unpackbits(data, bitorder="little")[: N * k])
