@@ -248,20 +248,24 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
 
 // ---------------------------------------------------------------------------
 // Packet decode.  A warp stages a BATCH of G consecutive packets in shared
-// memory (TMA bulk, double-buffered) and decodes it in three passes:
+// memory (TMA bulk, double-buffered) and decodes it in passes:
+//   S  (syndrome, the checksum vector, P:L160) -- per (packet, segment) item,
+//      by a group of L lanes: s = XOR_j [32 j * parity(x_j)] ^ S5(XOR_j x_j);
+//      the item's lead lane then writes the syndrome, the packet status and
+//      the counts, applies a correctable s as a flip of the STREAM bit at
+//      position s, and -- with HX (every k >= 96) -- compacts the segment's
+//      head in place (the 57 data bits of positions 0..63 moved to 7..63) and
+//      assembles the message word straddling the segment's start;
 //   R  (redundancy removal + merger) -- one lane per 32-bit
 //      message word.  The geometry is the same for every packet, so the host
 //      precomputes, per message word, where its bits sit in the packet stream
-//      as "pieces": maximal slices that stay inside one run (positions
-//      2^j+1 .. 2^(j+1)-1) of one segment.  From data index 57 on a run is
-//      >= 63 bits long, so almost every word is one or two slices: two funnel
-//      shifts and one merge.  The few words near a segment head (data index
-//      < 57: runs of 1, 3, 7, 15, 31 bits) or across a segment boundary are
-//   H  ("head" words) built by one lane each from their piece list;
-//   S  (syndrome, the checksum vector, P:L160) -- per (packet, segment) item,
-//      by a group of L lanes: s = XOR_j [32 j * parity(x_j)] ^ S5(XOR_j x_j);
-//      a correctable s flips the corrected data bit of the message in place.
-// Every message word is written exactly once (R or H), so nothing is zeroed.
+//      as slices that stay inside one run (positions 2^j+1 .. 2^(j+1)-1) of
+//      one segment.  From data index 57 on (after HX: everywhere) a run is
+//      >= 57 bits long, so a word is one or two slices: two funnel shifts and
+//      one merge.  "Head words" -- across a segment boundary, or without HX
+//      near a segment head (runs of 1, 3, 7, 15, 31 bits) -- are skipped and
+//   H  (only without HX) built by one lane each from their piece list.
+// Every message word is written exactly once (X, R or H), so nothing is zeroed.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kPktMaxWords = kPktMaxMsgBytes / 4;
 #ifndef HAM_PKT_STAGES
@@ -278,7 +282,7 @@ constexpr uint32_t kPktMaxPieces = 640;
 struct PacketTables {
   uint32_t Wp;                    // message words per packet, ceil(msg_bytes / 4)
   uint32_t n_special, n_pieces;
-  uint32_t mag_t, mag_ns, mag_wp, mag_np;  // floor(2^32 / d), d = t, n_special, Wp, n_pieces (divmod_small)
+  uint32_t mag_t, mag_ns;  // floor(2^32 / d), d = t, n_special (divmod_small)
   uint32_t headx;                 // 1: segment heads are compacted in place first (pass X, kPktHeadxMinK)
   uint32_t Wfull, rem, mag_rem;   // pass R: Wp = Wfull + rem, Wfull a multiple of 32; floor(2^32 / rem)
   // src0 (bits 0..15) | nb0 (bits 16..21): a word is slice 0 (nb0 bits) and, if nb0 < 32, slice 1 =
@@ -386,8 +390,6 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
   auto mag = [](uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : static_cast<uint32_t>((1ull << 32) / d); };
   T.mag_t = mag(g.t);
   T.mag_ns = mag(T.n_special);
-  T.mag_wp = mag(T.Wp);
-  T.mag_np = mag(T.n_pieces);
   T.Wfull = T.Wp / 32 * 32;
   T.rem = T.Wp - T.Wfull;
   T.mag_rem = mag(T.rem);
