@@ -311,12 +311,12 @@ uint32_t host_run_of(uint32_t d) {
 // two lanes rewrite the same stream word: k >= 96 gives n >= 103.
 constexpr uint32_t kPktHeadxMinK = 96;
 
-hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
+hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T, bool allow_headx = true) {
   const uint32_t bits = g.msg_bytes * 8u;
   T.Wp = (g.msg_bytes + 3) / 4;
   uint32_t kmin = ~0u;
   for (uint32_t i = 0; i < g.t; ++i) kmin = std::min(kmin, g.k[i]);
-  T.headx = kmin >= kPktHeadxMinK ? 1u : 0u;
+  T.headx = (allow_headx && kmin >= kPktHeadxMinK) ? 1u : 0u;
   T.n_special = 0;
   T.n_pieces = 0;
   uint32_t seg = 0;
@@ -384,7 +384,7 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T) {
           }
         }
       }
-      if (!ok) return set_err(HAMMING_E_ARG, "packets: unexpected head word layout");
+      if (!ok) return build_packet_tables(g, T, false);  // not expected; decode without pass X
     }
   }
   auto mag = [](uint32_t d) { return d <= 1 ? 0xFFFFFFFFu : static_cast<uint32_t>((1ull << 32) / d); };
