@@ -26,18 +26,25 @@ for m in (2, 3, 4, 5, 6):
     ham.decode_host(m, rx, N, torch.empty(ham.data_bytes(m, N), dtype=torch.uint8),
                     torch.empty(N, dtype=torch.uint8), ws, chunk_codewords=2048, n_streams=2)
 # SECDED, long perfect codes, the paper's packets
-for m in (3, 6):
+for m in (3, 4, 5, 6):
     for N in (1, 3 * 1024 + 77):
         rx = ham.channel_generate_secded(m, 5, 0, N, p=0.5, q2=0.5)
-        ham.decode_secded(m, rx, N)
+        res = ham.decode_secded(m, rx, N)
+        data = torch.empty(ham.data_bytes(m, N), dtype=torch.uint8, device="cuda")
+        data.copy_(res.data[: data.numel()])
+        ham.encode_secded(m, data, N)
         torch.cuda.synchronize()
 for m in (7, 8):
     for N in (1, 128 * 5 + 3):
         rx = torch.randint(0, 256, (ham.coded_bytes(m, N),), dtype=torch.uint8, device="cuda")
         ham.decode(m, rx, N)
         torch.cuda.synchronize()
-for M, t in ((400, 6), (2000, 2), (13, 3)):
+# packets: with head compaction (k >= 96: 400/6, 400/5, 2000/2, 1200/3, 97/8) and without (13/3,
+# 71/6), several launch shapes (8, 12, 16 warps; 1..10 packets per batch), uncorrectable segments
+for M, t in ((400, 6), (400, 5), (2000, 2), (1200, 3), (97, 8), (13, 3), (71, 6)):
     rx, _ = ham.packet_channel_generate(M, t, 1, 0, 37, p=1.0)
     ham.decode_packets(M, t, rx, 37)
+    noise = torch.randint(0, 256, rx.shape, dtype=torch.uint8, device="cuda")
+    ham.decode_packets(M, t, noise, 37)
     torch.cuda.synchronize()
 print("sanitize workload done")
