@@ -29,11 +29,20 @@ def code_nk(m: int) -> tuple[int, int]:
 
 
 def coded_bytes(m: int, n_codewords: int) -> int:
-    return int(lib().hamming_coded_bytes(m, n_codewords))
+    """ceil(n N / 8) -- the same value as the C ABI's hamming_coded_bytes (tested), computed here
+    so the per-call path makes no extra foreign calls."""
+    n, N = (1 << m) - 1, int(n_codewords)
+    if not 2 <= m <= 8 or N > ((1 << 64) - 1) // n:
+        return 0
+    return (n * N + 7) >> 3
 
 
 def data_bytes(m: int, n_codewords: int) -> int:
-    return int(lib().hamming_data_bytes(m, n_codewords))
+    """ceil(k N / 8), as hamming_data_bytes."""
+    n, N = (1 << m) - 1, int(n_codewords)
+    if not 2 <= m <= 8 or N > ((1 << 64) - 1) // n:
+        return 0
+    return ((n - m) * N + 7) >> 3
 
 
 def channel_thresholds(p: float, q2: float) -> tuple[int, int, int]:
@@ -53,15 +62,22 @@ def _dev_ptr(t: Optional[torch.Tensor], name: str, min_bytes: int):
         raise ValueError(f"{name} must be a CUDA tensor")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
-    if t.numel() * t.element_size() < min_bytes:
-        raise ValueError(f"{name} holds {t.numel() * t.element_size()} bytes, needs {min_bytes}")
-    return ctypes.c_void_p(t.data_ptr())
+    if t.nbytes < min_bytes:
+        raise ValueError(f"{name} holds {t.nbytes} bytes, needs {min_bytes}")
+    return t.data_ptr()  # an int; the argtypes make it a void*
 
 
-def _stream_handle(stream, device) -> ctypes.c_void_p:
-    if stream is None:
-        stream = torch.cuda.current_stream(device)
-    return ctypes.c_void_p(stream.cuda_stream)
+# torch's current raw cudaStream_t without building a Stream object (a few us per call on the
+# latency-bound small-packet path); the public API is the fallback
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream_handle(stream, device):
+    if stream is not None:
+        return stream.cuda_stream
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 @dataclass

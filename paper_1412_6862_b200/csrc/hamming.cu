@@ -1711,11 +1711,16 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
   if (N < kSmallPacketCw) {
     // Small packets are latency-bound: a light CTA (4 warps, 2 stages, no
-    // table to build or copy) launches and finishes fastest.
+    // table to build or copy) launches and finishes fastest; from 4 full tiles
+    // on, 8 warps, so that the ragged tail gets a warp of its own instead of
+    // queueing behind a full tile (C1, a 4 KB (7,4) packet: 6.2 -> 4.0 us per
+    // packet in a CUDA graph).
     switch (m) {
-#define HAMMING_SMALL_CASE(MM) \
-  case MM:                     \
-    return Launcher<DecodeOp<MM>, 4, 2, true>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
+#define HAMMING_SMALL_CASE(MM)                                                                               \
+  case MM:                                                                                                   \
+    return N >= 4 * kTileCw                                                                                  \
+               ? Launcher<DecodeOp<MM>, 8, 2, true>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate) \
+               : Launcher<DecodeOp<MM>, 4, 2, true>::run(in, out, syn, N, ib, ob, counter, {}, st, accumulate);
       HAMMING_SMALL_CASE(2)
       HAMMING_SMALL_CASE(3)
       HAMMING_SMALL_CASE(4)

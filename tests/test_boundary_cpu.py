@@ -49,6 +49,12 @@ def test_abi_and_sizes(L):
             assert ham.data_bytes(m, N) == (k * N + 7) // 8
     assert ham.coded_bytes(9, 10) == 0 and ham.coded_bytes(1, 10) == 0
     assert ham.coded_bytes(6, 2 ** 64 // 63 + 1) == 0      # overflow
+    # the binding computes the sizes in Python: the same values as the C ABI's helpers
+    for m in (1, 2, 3, 6, 8, 9):
+        for N in (0, 1, 4681, 10 ** 12, 2 ** 64 // 63, 2 ** 64 // 63 + 1, 2 ** 64 // 255 + 1):
+            N = min(N, 2 ** 64 - 1)
+            assert ham.coded_bytes(m, N) == L.hamming_coded_bytes(m, N), (m, N)
+            assert ham.data_bytes(m, N) == L.hamming_data_bytes(m, N), (m, N)
     # the north-star shapes: a 4 KB (7,4) packet is 4681 codewords
     assert ham.coded_bytes(3, 4681) == 4096
 
