@@ -448,6 +448,7 @@ def main_packets(args):
     if world > 1:
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
+    l2_bytes = getattr(torch.cuda.get_device_properties(torch.cuda.current_device()), "L2_cache_size", 126 << 20)
     dev = torch.device("cuda", torch.cuda.current_device())
     a, b = ham.shard_range(P, rank, world, align=1)
     p_loc = b - a
@@ -490,7 +491,7 @@ def main_packets(args):
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic: seeded packet channel on the device",
         "config": {"workload": desc, "M": M, "t": t, "packets": P, "coded_bytes_per_packet": cb,
-                   "parallelism": f"dp{world} (packet-range shards)", "l2": "inputs larger than L2" if P * stride > 2**28
+                   "parallelism": f"dp{world} (packet-range shards)", "l2": "inputs larger than L2" if P * stride > l2_bytes
                    else "L2-resident inputs (warm)"},
         "roofline": {"bound": "hbm", "achieved": round(alg / (kms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(alg / (kms / 1e3) / 1e9 / peak, 4), "traffic": None,
