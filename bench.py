@@ -377,7 +377,7 @@ def run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank):
     del rx_d
     data_h = torch.empty(ham.data_bytes(m, n_loc), dtype=torch.uint8, pin_memory=True)
     syn_h = torch.empty(n_loc, dtype=torch.uint8, pin_memory=True)
-    chunk = 1 << 22
+    chunk = 1 << 24  # tools/e2e_sweep.py: 2^24 codewords x 3 streams is the best of 2^22..2^25 x 2..4 (link-bound)
     ws = torch.empty(ham.host_workspace_bytes(m, chunk, 3, True), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     ham.decode_host(m, rx_h, n_loc, data_h, syn_h, ws, chunk_codewords=chunk, n_streams=3)
