@@ -573,7 +573,8 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
     const bool head = nb > 32;  // head words: pass R skips them (pass H, or with HX pass X, writes them)
-    wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, head ? 0u : 0xFFFFFFFFu);
+    // .w: the shift of slice 1 (1..32, the skipped parity bit), 0 for a head word (pass R skips it)
+    wdesc[i] = make_uint4(s0 >> 5, s0 & 31u, nb >= 32 ? 0xFFFFFFFFu : (1u << nb) - 1u, head ? 0u : (s0 & 31u) + 1u);
   }
   for (uint32_t i = threadIdx.x; i < T.n_pieces; i += blockDim.x) pieces[i] = make_uint2(T.piece[i], T.piece_word[i]);
   for (uint32_t i = threadIdx.x; i < T.n_special; i += blockDim.x)
@@ -703,17 +704,17 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         for (uint32_t W = lane; W < Wp; W += 32) {
           const uint4 d = wdesc[W];
           const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
-          if (d.w) mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+          if (d.w) mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
         }
       } else {
         for (uint32_t W = lane; W < T.Wfull; W += 32) {
-          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, 0 for a head word}
+          const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, shift + 1 (0: head word)}
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
           uint32_t* mp = mbuf + W;
           for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
             const uint32_t a0 = wp[0], a1 = wp[1];
             // slice 1 is the stream one bit further on (the parity position skipped)
-            if (d.w) *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+            if (d.w) *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
           }
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];
           const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          if (d.w) mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.y + 1) & ~d.z);
+          if (d.w) mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
         }
       }
     }
