@@ -500,13 +500,15 @@ __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t
   const uint32_t full = active ? (n + 1) / 64 : 0;  // full 64-position chunks
   const uint32_t* wq = w + (o >> 5) + 2 * q;
   uint32_t X = 0, H = 0, A0 = 0, A1 = 0, BB = 0;
-  for (uint32_t blk = 0; 4 * L * blk < full; ++blk) {
+  // one block = 4 chunks per lane; blocks below full / 4L are complete for every lane of the
+  // group, so only the last, partial block tests which of its chunks exist
+  auto block = [&](uint32_t blk, auto checked) {
     const uint32_t* wb = wq + 8 * L * blk;
     const int cnt = static_cast<int>(full - 4 * L * blk) - static_cast<int>(q);
     uint32_t Xb = 0;
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
-      if (static_cast<int>(L) * it < cnt) {
+      if (!decltype(checked)::value || static_cast<int>(L) * it < cnt) {
         const uint32_t w0 = wb[2 * L * it], w1 = wb[2 * L * it + 1], w2 = wb[2 * L * it + 2];
         const uint32_t hi = __funnelshift_r(w1, w2, rb);
         const uint32_t y = __funnelshift_r(w0, w1, rb) ^ hi;
@@ -518,7 +520,10 @@ __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t
     }
     X ^= Xb;
     BB ^= (__popc(Xb) & 1u) ? blk : 0u;
-  }
+  };
+  const uint32_t nb = full / (4 * L);
+  for (uint32_t blk = 0; blk < nb; ++blk) block(blk, std::false_type{});
+  if (4 * L * nb < full) block(nb, std::true_type{});
   uint32_t P = (64u * ((q * (__popc(X) & 1u)) ^ L * ((4u * BB) ^ (__popc(A0) & 1u) ^ ((__popc(A1) & 1u) << 1)))) ^
                (32u * (__popc(H) & 1u));
   if (active && q == 0) {  // the tail: positions 64 full .. n (fewer than 64)
