@@ -623,6 +623,10 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     }
   }
   __syncwarp();
+  // contiguous 16-byte-aligned messages leave by one TMA bulk store per batch (decided once:
+  // with msg_bytes a multiple of 16 every batch's start stays aligned)
+  const bool bulk_out = a.out_stride == g.msg_bytes && (g.msg_bytes & 15u) == 0 &&
+                        (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0;
   uint32_t it = 0;
   for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
     const uint32_t buf = it % kPktStages;
@@ -765,7 +769,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     // write the batch's messages (packet pk at word pk * Wp of mbuf) and statuses
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
     const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + p0 * a.out_stride);
-    if (a.out_stride == g.msg_bytes && (g.msg_bytes & 15u) == 0 && (ob & 15u) == 0) {
+    if (bulk_out) {
       fence_proxy_async_smem();  // this lane's st.shared / atomics visible to the bulk copy
       __syncwarp();
       if (lane == 0) {
