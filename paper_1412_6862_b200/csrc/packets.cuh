@@ -678,13 +678,15 @@ __global__ void __launch_bounds__(kPktWarps * 32)
             uint32_t* wq = wm + (o >> 5);
             const uint32_t r = o & 31u;
             const uint32_t w0 = wq[0], w1 = wq[1], w2 = wq[2];
-            const uint64_t x = static_cast<uint64_t>(__funnelshift_r(w0, w1, r)) |
-                               (static_cast<uint64_t>(__funnelshift_r(w1, w2, r)) << 32);  // bit p = position p
-            // data positions 3, 5..7, 9..15, 17..31, 33..63 -> bits 0..56 (the m = 6 compaction, App. A)
-            const uint64_t d = ((x >> 3) & 0x1ull) | ((x >> 4) & 0xeull) | ((x >> 5) & 0x7f0ull) |
-                               ((x >> 6) & 0x3fff800ull) | ((x >> 7) & 0x1fffffffc000000ull);
-            const uint64_t xn = (x & 0x7full) | (d << 7);  // positions 0..6 kept, data at 7..63
-            const uint32_t lo = static_cast<uint32_t>(xn), hi = static_cast<uint32_t>(xn >> 32);
+            // bit p of (x0, x1) = position p (p < 32 in x0)
+            const uint32_t x0 = __funnelshift_r(w0, w1, r), x1 = __funnelshift_r(w1, w2, r);
+            // data positions 3, 5..7, 9..15, 17..31, 33..63 -> bits 0..56 (the m = 6 compaction,
+            // App. A) in 32-bit halves: d0 = bits 0..31 (positions 3..38), d1 = bits 32..56 (39..63)
+            const uint32_t d0 = ((x0 >> 3) & 0x1u) | ((x0 >> 4) & 0xeu) | ((x0 >> 5) & 0x7f0u) |
+                                ((x0 >> 6) & 0x3fff800u) | ((x1 << 25) & 0xfc000000u);
+            const uint32_t d1 = x1 >> 7;
+            // positions 0..6 kept, data at 7..63
+            const uint32_t lo = (x0 & 0x7fu) | (d0 << 7), hi = (d0 >> 25) | (d1 << 7);
             const uint32_t lm = (1u << r) - 1u;
             // plain read-modify-write: with k >= 96 no other item's head window or flip shares these
             // words in this round, and the bits outside positions 7..63 are written back unchanged
@@ -700,7 +702,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
               const uint32_t m0 = __funnelshift_lc(0xFFFFFFFFu, 0u, nb0);
               const uint32_t tail = ((__funnelshift_r(a0, a1, s0) & m0) | (__funnelshift_rc(a0, a1, (s0 & 31u) + 1) & ~m0)) &
                                     __funnelshift_lc(0xFFFFFFFFu, 0u, lt);
-              mbuf[pk * Wp + W] = tail | (static_cast<uint32_t>(d) << lt);
+              mbuf[pk * Wp + W] = tail | (d0 << lt);
             }
           }
         }
