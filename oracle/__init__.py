@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_encode.argtypes = [ctypes.c_int, ctypes.c_void_p, u64, ctypes.c_void_p]
         L.oracle_generate.argtypes = [ctypes.c_int, u64, u64, u64, u64, ctypes.c_int, u64,
                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_count_events.argtypes = [u64, u64, u64, u64, ctypes.c_int, u64, ctypes.POINTER(u64),
+                                          ctypes.POINTER(u64)]
         u32p = ctypes.POINTER(ctypes.c_uint32)
         L.oracle_packet_layout.argtypes = [ctypes.c_uint32, ctypes.c_int, u32p, u32p]
         L.oracle_packet_layout.restype = ctypes.c_long
@@ -237,6 +239,25 @@ def generate(m: int, seed: int, c_first: int, count: int, p: float = 0.1, q2: fl
     with ThreadPoolExecutor(max(1, threads)) as ex:
         list(ex.map(run, _ranges(count, threads)))
     return rx, sent, err
+
+
+def count_events(seed: int, c_first: int, count: int, p: float = 0.1, q2: float = 0.0, threads: int = 1):
+    """(events, weight-2 events) of the seeded channel over global codewords
+    c_first .. c_first + count - 1 -- the draws of generate() alone, for
+    packets too large to generate on the host.  Independent of m."""
+    thresh, all_, q2t = channel_thresholds(p, q2)
+    L = lib()
+
+    def run(r):
+        a, b = r
+        ev, w2 = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        L.oracle_count_events(seed & (2 ** 64 - 1), c_first + a, b - a, thresh, all_, q2t, ctypes.byref(ev),
+                              ctypes.byref(w2))
+        return int(ev.value), int(w2.value)
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        res = list(ex.map(run, _ranges(count, threads, align=1)))
+    return sum(r[0] for r in res), sum(r[1] for r in res)
 
 
 # ------------------------------------------------ packets (the paper's workload)

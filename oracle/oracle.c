@@ -319,6 +319,29 @@ int oracle_generate(int m, uint64_t seed, uint64_t c_first, uint64_t count,
     return 0;
 }
 
+/* The channel's error events alone, for packets too large to generate on the
+ * host (C5: 8.7e9 codewords): the draws u(c,1) and u(c,2) of
+ * oracle_generate, nothing else.  *events = #{c : all or u(c,1) < thresh},
+ * *weight2 (nullable) = how many of them have (u(c,2) >> 32) < q2thresh.
+ * With q2 = 0 every event is one flip, whose syndrome is the flipped
+ * position (nonzero), so a decoder's corrected count must equal *events.
+ * Returns 0. */
+int oracle_count_events(uint64_t seed, uint64_t c_first, uint64_t count, uint64_t thresh, int all,
+                        uint64_t q2thresh, uint64_t *events, uint64_t *weight2)
+{
+    uint64_t ev = 0, w2 = 0;
+    for (uint64_t i = 0; i < count; i++) {
+        uint64_t c = c_first + i;
+        if (all || draw(seed, c, 1) < thresh) {
+            ev++;
+            if ((draw(seed, c, 2) >> 32) < q2thresh) w2++;
+        }
+    }
+    *events = ev;
+    if (weight2) *weight2 = w2;
+    return 0;
+}
+
 /* ABI marker so tests can check they loaded the oracle, not something else. */
 int oracle_version(void) { return 1; }
 

@@ -30,9 +30,16 @@ MUTANTS = [
     ("splitmix constant typo", "z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;", "z = (z ^ (z >> 27)) * 0x94D049BB133111EAULL;"),
     ("packet layout: larger segments last", "uint32_t k = msg_bits / (uint32_t)t + ((uint32_t)i < msg_bits % (uint32_t)t ? 1u : 0u);", "uint32_t k = msg_bits / (uint32_t)t + ((uint32_t)(t - 1 - i) < msg_bits % (uint32_t)t ? 1u : 0u);"),
     ("packet: uncorrectable segment still flipped", "        if (s != 0 && s <= n) {                                                         /* EC */", "        if (s != 0 && s <= 2 * n) {                                                     /* EC */"),
+    ("packet generator flips p+1", "uint64_t b = cb + p - 1;", "uint64_t b = cb + p;"),
+    ("packet generator event draw index off by one", "uint64_t ue = mix64(key + ((uint64_t)W + 2 * (uint64_t)i + 1) * 0x9E3779B97F4A7C15ULL);", "uint64_t ue = mix64(key + ((uint64_t)W + 2 * (uint64_t)i) * 0x9E3779B97F4A7C15ULL);"),
+    ("packet generator message key g instead of g+1", "uint64_t key = mix64(seed + (g + 1) * 0x9E3779B97F4A7C15ULL);", "uint64_t key = mix64(seed + g * 0x9E3779B97F4A7C15ULL);"),
+    ("count_events uses the message draw", "if (all || draw(seed, c, 1) < thresh) {\n            ev++;", "if (all || draw(seed, c, 0) < thresh) {\n            ev++;"),
+    ("count_events weight-2 test on the low half", "if ((draw(seed, c, 2) >> 32) < q2thresh) w2++;", "if ((draw(seed, c, 2) & 0xFFFFFFFFULL) < q2thresh) w2++;"),
+    ("generator p1 from the high half", "p1 = 1 + (int)((w3 * (uint64_t)n) >> 32);", "p1 = 1 + (int)((w4 * (uint64_t)n) >> 32);"),
 ]
 
-TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_generator.py", "tests/test_oracle_packets.py"]
+TESTS = ["tests/test_oracle_pins.py", "tests/test_oracle_generator.py", "tests/test_oracle_packets.py",
+         "tests/test_oracle_draws.py"]
 
 
 def main():
