@@ -15,6 +15,17 @@ the NCCL all_reduce of the 8-byte corrected count.  Inputs are generated on
 the device by the library's seeded channel generator (p = 0.1 single-bit
 errors) and are far larger than L2, so no flush is needed.
 
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset) the script
+re-launches itself as N ranks through torch.distributed.run (127.0.0.1), so
+`python bench.py --gpus 8` and the torchrun form run the same thing; every
+rank asserts world size == --gpus.  NCCL logs its communicator init
+(NCCL_DEBUG=INFO, INIT subsystem) to stderr, and rank 0 prints the
+communicator's size after a warm-up all_reduce.
+
+Single-GPU runs (N = 1) also time the driver-visible sweeps of BASELINE.json's
+other configs (C1 latency, C2 sizes cold and warm, C3 every m, C4 every p) into
+the "sweeps" field of the same JSON line (--no-sweeps skips them).
+
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
 paper-derived checker, as it stands) on the host cores instead.
 """
@@ -69,16 +80,24 @@ REASON_FIELDS = ["clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_th
 
 
 class ClockSampler:
-    """nvidia-smi sampled every 100 ms while the timed region runs."""
+    """nvidia-smi sampled every 100 ms; each row is stamped with the host time it
+    arrived, so the statistics cover the timed region only (stop(region=...))."""
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self.proc = None
         self.thread = None
+        self.power_field = "power.draw"
 
     def start(self):
-        q = "clocks.sm,clocks.max.sm," + ",".join(REASON_FIELDS) + ",clocks.mem,power.draw"
+        try:  # the instantaneous reading where the driver has it (power.draw averages over ~1 s)
+            if subprocess.run(["nvidia-smi", f"--id={self.index}", "--query-gpu=power.draw.instant",
+                               "--format=csv,noheader,nounits"], capture_output=True, timeout=10).returncode == 0:
+                self.power_field = "power.draw.instant"
+        except Exception:
+            pass
+        q = "clocks.sm,clocks.max.sm," + ",".join(REASON_FIELDS) + ",clocks.mem," + self.power_field
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -94,9 +113,9 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 4 + len(REASON_FIELDS):
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
 
-    def stop(self):
+    def stop(self, region=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -107,22 +126,26 @@ class ClockSampler:
             self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        rows = [r for t, r in self.rows if region is None or region[0] <= t <= region[1] + 0.1]
+        if not rows:  # a region shorter than the sampling period: the nearest samples
+            rows = [r for _, r in self.rows]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for name, val in zip(REASON_FIELDS, r[2:]):
                 if val.lower() == "active":
                     reasons.add(name.split(".")[-1])
 
         def med(col):
-            v = sorted(float(r[col]) for r in self.rows if r[col].replace(".", "").isdigit())
+            v = sorted(float(r[col]) for r in rows if r[col].replace(".", "").isdigit())
             return v[len(v) // 2] if v else None
 
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows),
-                "mem_mhz": med(2 + len(REASON_FIELDS)), "power_w": med(3 + len(REASON_FIELDS))}
+                "reasons": sorted(reasons), "samples": len(rows),
+                "mem_mhz": med(2 + len(REASON_FIELDS)), "power_w": med(3 + len(REASON_FIELDS)),
+                "power_field": self.power_field}
 
 
 # ------------------------------------------------------------- cpu baseline
@@ -138,16 +161,24 @@ def cpu_oracle_run(m: int, p: float, q2: float, n_cw: int, threads: int):
 
 
 def cpu_baseline(m, p, q2, threads, target_s=1.0):
+    """The oracle as it stands on all host threads (~target_s of wall time) and
+    on one thread (~target_s / 2), on a seeded prefix of the same workload."""
     n = (1 << m) - 1
     probe = 1 << 15
     t, _ = cpu_oracle_run(m, p, q2, probe, threads)
     n_cw = int(min(1 << 26, max(probe, probe * target_s / max(t, 1e-6)))) // 1024 * 1024
     t, _ = cpu_oracle_run(m, p, q2, n_cw, threads)
     gbps = n * n_cw / t / 1e9
+    t1, _ = cpu_oracle_run(m, p, q2, probe, 1)
+    n1 = int(min(1 << 24, max(probe, probe * target_s / 2 / max(t1, 1e-6)))) // 1024 * 1024
+    t1, _ = cpu_oracle_run(m, p, q2, n1, 1)
     return {"value": round(gbps, 4), "unit": "coded Gbit/s", "cores": threads, "kind": "oracle",
             "sample": f"first {n_cw} codewords of the workload (same m, p, q2, seed), {n * n_cw / 8 / 2**20:.0f} MiB "
                       f"coded, decoded by the plain C oracle on {threads} host threads in {t:.2f} s "
-                      f"({t * threads:.0f} CPU-s)"}
+                      f"({t * threads:.0f} CPU-s)",
+            "value_1thread": round(n * n1 / t1 / 1e9, 5),
+            "sample_1thread": f"first {n1} codewords on 1 thread in {t1:.2f} s",
+            "cpu_model": cpu_model()}
 
 
 # ------------------------------------------------------------------- main
@@ -166,6 +197,7 @@ def parse():
     ap.add_argument("--no-syndromes", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip the C1..C4 sweeps of a single-GPU run")
     ap.add_argument("--e2e-gib", type=float, default=8.0, help="host-buffer e2e packet size (GiB coded)")
     return ap.parse_args()
 
@@ -179,6 +211,43 @@ def workload(args, world):
         bits *= world
     N = bits // n
     return cfg, m, n, N
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_command(args_argv, gpus: int, port: int) -> list:
+    """The torch.distributed.run command that runs this script as `gpus` ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *args_argv]
+
+
+def maybe_relaunch(args) -> None:
+    """--gpus N > 1 without a torchrun environment: run N ranks of this script
+    (one per GPU) and exit with their status."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = relaunch_command(sys.argv[1:], args.gpus, free_port())
+    log("[bench] relaunching as", args.gpus, "ranks:", " ".join(cmd))
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -215,7 +284,7 @@ def run_reference(args):
         "config": {"workload": cfg["desc"], "m": m, "n_codewords": N, "p": cfg["p"], "q2": cfg["q2"],
                    "parallelism": "host threads", "sample_codewords": n_cw},
         "cpu_baseline": {"value": round(value, 4), "unit": "coded Gbit/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 4), "unit": "coded Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -229,6 +298,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    maybe_relaunch(args)
 
     import torch
     import torch.distributed as dist
@@ -238,16 +308,32 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: world size {world} != --gpus {args.gpus}")
+    comm = None
     if world > 1:
         # HAMMING_BENCH_BACKEND=gloo (testing only): run the N > 1 path with several ranks on
         # however many GPUs the box has (ranks share a GPU), e.g. 2 ranks on a 1-GPU box
         backend = os.environ.get("HAMMING_BENCH_BACKEND", "nccl")
+        if backend == "nccl" and torch.cuda.device_count() < world:
+            raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, this box has "
+                             f"{torch.cuda.device_count()}")
         local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
         torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        # force the communicator up now (NCCL creates it lazily) and record what it spans
+        probe = torch.ones(1, dtype=torch.int64, device=torch.device("cuda", local))
+        dist.all_reduce(probe)
+        torch.cuda.synchronize()
+        comm = {"backend": backend, "world_size": dist.get_world_size(), "ranks_reduced": int(probe.item())}
+        if backend == "nccl":
+            comm["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+        log(f"[bench] rank {rank}: {backend} communicator up, world {comm['world_size']}, "
+            f"all_reduce(1) = {comm['ranks_reduced']}, device cuda:{local}")
+        assert comm["ranks_reduced"] == world
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -285,6 +371,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    host_t0 = time.time()
     ev_start.record(stream)
     for i in range(args.steps):
         kev[i][0].record(stream)
@@ -294,9 +381,10 @@ def main():
             dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
     ev_end.record(stream)
     torch.cuda.synchronize()
+    host_t1 = time.time()
     if world > 1:
         dist.barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop(region=(host_t0, host_t1))
     t_ms = ev_start.elapsed_time(ev_end)
     k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
     t_tensor = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
@@ -311,7 +399,7 @@ def main():
     alg_bytes = ham.coded_bytes(m, n_loc) + ham.data_bytes(m, n_loc) + (0 if syn is None else n_loc) + 8
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
     peak, peak_src, mp = measured_peaks()
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
@@ -321,10 +409,18 @@ def main():
                 if v["m"] == m and v["syndromes"] == (syn is not None):
                     if v["n_codewords"] == n_loc:   # the very launch bench times
                         traffic = int(v["traffic"])
+                        traffic_src = "measured: " + v["source"]
                     else:                            # same kernel, other size: per algorithmic byte
                         traffic = round(v["traffic_per_alg_byte"] * alg_bytes)
+                        traffic_src = (f"EXTRAPOLATED: ncu DRAM bytes per algorithmic byte "
+                                       f"({v['traffic_per_alg_byte']:.5f}) of the N = {v['n_codewords']} launch "
+                                       f"x this launch's algorithmic bytes")
         except Exception:
-            traffic = None
+            traffic, traffic_src = None, None
+    energy = None
+    if clocks.get("power_w"):
+        energy = {"power_w": clocks["power_w"], "pj_per_alg_byte": round(clocks["power_w"] / (achieved * 1e9) * 1e12, 1),
+                  "note": "board power (nvidia-smi, median over the timed region) / achieved algorithmic bandwidth"}
 
     result = {
         "metric": "coded Gbit/s decoded (device-timed, max over ranks)",
@@ -338,18 +434,25 @@ def main():
                    "syndromes": syn is not None, "parallelism": f"dp{world} (codeword-range shards)",
                    "l2": "inputs larger than L2 (no flush needed)", "grid_blocks": grid},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": f"tiles_kernel decode m={m} (one launch + 8-byte memset per hamming_decode call)",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": f"tiles_kernel decode m={m} (one launch per hamming_decode call)",
+                     "launches_per_call": launches_per_step,
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": round(k_ms, 4), "peak_source": peak_src},
         "clocks": clocks,
+        "energy": energy,
         "gpu_launches": launches_per_step * args.steps,
     }
+    if comm is not None:
+        result["comm"] = comm
 
     # ---- e2e: the same metric through the public host-buffer C-ABI call
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank)
     del rx, data, syn
     torch.cuda.empty_cache()
+
+    if world == 1 and not args.no_sweeps:
+        result["sweeps"] = run_sweeps(ham, torch, dev, peak)
 
     if rank == 0 and not args.no_cpu:
         try:
@@ -361,6 +464,182 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+C4_P = [0.0, 1e-3, 1e-2, 0.1, 0.25, 0.5, 0.75, 1.0]
+C2_SIZES = [1 << e for e in range(10, 27)] + [400, 800, 1200, 1600, 2000]
+
+
+def _median(xs):
+    xs = sorted(xs)
+    return xs[len(xs) // 2]
+
+
+def run_sweeps(ham, torch, dev, peak):
+    """BASELINE.json's other configs, timed in the same run on the same GPU
+    (device time, CUDA events on the launching stream):
+      c3: 256 MiB per call, every m, with and without syndromes -- median of
+          20 back-to-back calls alternating between two buffer sets (cold by
+          size: 0.55-0.73 GB moved per call vs a 126 MB L2);
+      c4: (31,26) 1 GiB, q2 = 0.25, every p -- median of 10 calls; the
+          branch-free decoder should be flat in p ("spread");
+      c2: (15,11) packets of 1 KiB..64 MiB + the paper's 400..2000 B, single
+          calls: "cold" = L2 flushed (256 MiB written) before each call, "warm"
+          = the same packet decoded just before; a queued sleep kernel keeps
+          host enqueue time out of both; median of 30;
+      c1: (7,4) 4 KB, single-call cold/warm latency as c2, plus 1000 calls on
+          1000 distinct packets captured in one CUDA graph (L2-resident,
+          labelled "warm")."""
+    st = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    out = {"method": run_sweeps.__doc__.split("\n", 1)[1].strip()}
+
+    def alg(m, N, syn=True):
+        return ham.coded_bytes(m, N) + ham.data_bytes(m, N) + (N if syn else 0) + 8
+
+    # ---- C3: every m at 256 MiB
+    pts = []
+    for m in (3, 4, 5, 6):
+        n, k = ham.code_nk(m)
+        N = (256 << 20) * 8 // n
+        sets = []
+        for b in range(2):
+            rx = ham.channel_generate(m, SEED ^ (m << 4) ^ b, 0, N, p=0.1, device=dev)
+            sets.append((rx, torch.empty(ham.data_bytes(m, N), dtype=torch.uint8, device=dev),
+                         torch.empty(N, dtype=torch.uint8, device=dev), torch.empty(1, dtype=torch.int64, device=dev)))
+        row = {"m": m, "n": n, "k": k, "n_codewords": N}
+        for syn_on in (True, False):
+            ts = []
+            for i in range(24):
+                rx, d, sy, c = sets[i & 1]
+                a, b = ev(), ev()
+                a.record(st)
+                ham.decode(m, rx, N, data_out=d, syndromes=sy if syn_on else False, corrected=c)
+                b.record(st)
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            t = _median([a.elapsed_time(b) for a, b in ts[4:]]) / 1e3
+            key = "" if syn_on else "_no_syndromes"
+            row["us_per_call" + key] = round(t * 1e6, 2)
+            row["coded_gbps" + key] = round(n * N / t / 1e9, 1)
+            row["frac" + key] = round(alg(m, N, syn_on) / t / 1e9 / peak, 4)
+        pts.append(row)
+        del sets
+    out["c3_code_length_256MiB"] = {"unit": "coded Gbit/s", "peak_gbs": peak, "points": pts}
+    torch.cuda.empty_cache()
+
+    # ---- C4: (31,26), 1 GiB, every p, q2 = 0.25
+    m, q2 = 5, 0.25
+    n, k = ham.code_nk(m)
+    N = (1 << 30) * 8 // n
+    rx = torch.empty(ham.coded_bytes(m, N), dtype=torch.uint8, device=dev)
+    d = torch.empty(ham.data_bytes(m, N), dtype=torch.uint8, device=dev)
+    sy = torch.empty(N, dtype=torch.uint8, device=dev)
+    c = torch.empty(1, dtype=torch.int64, device=dev)
+    pts = []
+    for p in C4_P:
+        ham.channel_generate(m, SEED ^ int(p * 1000), 0, N, p=p, q2=q2, rx_out=rx)
+        ts = []
+        for i in range(13):
+            a, b = ev(), ev()
+            a.record(st)
+            ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+            b.record(st)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        t = _median([a.elapsed_time(b) for a, b in ts[3:]]) / 1e3
+        pts.append({"p": p, "corrected": int(c.item()), "us_per_call": round(t * 1e6, 2),
+                    "coded_gbps": round(n * N / t / 1e9, 1), "frac": round(alg(m, N) / t / 1e9 / peak, 4)})
+    vals = [x["coded_gbps"] for x in pts]
+    out["c4_error_sweep_1GiB"] = {"unit": "coded Gbit/s", "q2": q2, "n_codewords": N, "points": pts,
+                                  "spread": round(max(vals) / min(vals) - 1, 4)}
+    del rx, d, sy, c
+    torch.cuda.empty_cache()
+
+    # ---- C2 / C1: single-call latency, cold (L2 flushed) and warm
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def single_calls(m, rx, N, d, sy, c, reps=30):
+        cold, warm = [], []
+        for _ in range(reps):
+            flush.zero_()
+            torch.cuda._sleep(20000)  # keep the stream busy while the host enqueues the call
+            a, b = ev(), ev()
+            a.record(st)
+            ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+            b.record(st)
+            torch.cuda._sleep(20000)
+            a2, b2 = ev(), ev()
+            a2.record(st)
+            ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+            b2.record(st)
+            cold.append((a, b))
+            warm.append((a2, b2))
+        torch.cuda.synchronize()
+        return (_median([a.elapsed_time(b) for a, b in cold]) / 1e3,
+                _median([a.elapsed_time(b) for a, b in warm]) / 1e3)
+
+    pts = []
+    m = 4
+    n, k = ham.code_nk(m)
+    for S in sorted(C2_SIZES):
+        N = S * 8 // n
+        rx = ham.channel_generate(m, SEED ^ S, 0, N, p=0.1, device=dev)
+        d = torch.empty(max(1, ham.data_bytes(m, N)), dtype=torch.uint8, device=dev)
+        sy = torch.empty(N, dtype=torch.uint8, device=dev)
+        c = torch.empty(1, dtype=torch.int64, device=dev)
+        ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+        tc, tw = single_calls(m, rx, N, d, sy, c)
+        pts.append({"coded_bytes": S, "n_codewords": N, "cold_us": round(tc * 1e6, 2), "warm_us": round(tw * 1e6, 2),
+                    "cold_coded_gbps": round(n * N / tc / 1e9, 2), "warm_coded_gbps": round(n * N / tw / 1e9, 2),
+                    "cold_frac": round(alg(m, N) / tc / 1e9 / peak, 4)})
+    out["c2_packet_size_15_11"] = {"unit": "coded Gbit/s", "points": pts,
+                                   "note": "single calls; % of HBM peak quoted from the cold series only"}
+
+    m, N = 3, 4681
+    n, k = ham.code_nk(m)
+    rx = ham.channel_generate(m, SEED, 0, N, p=0.1, device=dev)
+    d = torch.empty(ham.data_bytes(m, N), dtype=torch.uint8, device=dev)
+    sy = torch.empty(N, dtype=torch.uint8, device=dev)
+    c = torch.empty(1, dtype=torch.int64, device=dev)
+    ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+    tc, tw = single_calls(m, rx, N, d, sy, c, reps=100)
+    G = 1000
+    cbp = (ham.coded_bytes(m, N) + 255) // 256 * 256
+    dbp = (ham.data_bytes(m, N) + 255) // 256 * 256
+    sp = (N + 255) // 256 * 256
+    big = torch.empty(G * cbp, dtype=torch.uint8, device=dev)
+    big.view(G, cbp)[:, : ham.coded_bytes(m, N)] = rx[: ham.coded_bytes(m, N)]
+    bd = torch.empty(G * dbp, dtype=torch.uint8, device=dev)
+    bs = torch.empty(G * sp, dtype=torch.uint8, device=dev)
+    bc = torch.empty(G, dtype=torch.int64, device=dev)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(st)
+    with torch.cuda.stream(side):
+        for i in range(3):
+            ham.decode(m, big[i * cbp:], N, data_out=bd[i * dbp:], syndromes=bs[i * sp:], corrected=bc[i:i + 1])
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for i in range(G):
+                ham.decode(m, big[i * cbp:], N, data_out=bd[i * dbp:], syndromes=bs[i * sp:], corrected=bc[i:i + 1])
+    torch.cuda.synchronize()
+    g.replay()
+    tg = []
+    for _ in range(5):
+        a, b = ev(), ev()
+        a.record(st)
+        g.replay()
+        b.record(st)
+        torch.cuda.synchronize()
+        tg.append(a.elapsed_time(b) / 1e3 / G)
+    tb = min(tg)
+    out["c1_7_4_4KB"] = {"n_codewords": N, "cold_us": round(tc * 1e6, 2), "warm_us": round(tw * 1e6, 2),
+                         "graph_batched_us_per_packet": round(tb * 1e6, 3),
+                         "graph_batched_coded_gbps": round(n * N / tb / 1e9, 2),
+                         "note": "graph: 1000 distinct packets per replay, L2-resident (warm)"}
+    del flush, big, bd, bs, bc, g
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank):
@@ -394,11 +673,18 @@ def run_e2e(args, ham, torch, m, n, k, cfg, dev, world, rank):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = float(tt[0])
+    nbytes = torch.tensor([ham.coded_bytes(m, n_loc), ham.data_bytes(m, n_loc) + n_loc + 8], dtype=torch.int64,
+                          device=dev)
+    if world > 1:
+        dist.all_reduce(nbytes, op=dist.ReduceOp.SUM)
     out = {"value": round(n * N_e / t / 1e9, 2), "unit": "coded Gbit/s",
-           "h2d_bytes_per_step": ham.coded_bytes(m, n_loc),
-           "d2h_bytes_per_step": ham.data_bytes(m, n_loc) + n_loc + 8,
-           "workload": f"{args.e2e_gib:g} GiB coded packet of the same code/channel in pinned host memory, "
-                       f"hamming_decode_host (chunk {chunk} codewords, 3 streams), wall clock per call",
+           "h2d_bytes_per_step": int(nbytes[0]),
+           "d2h_bytes_per_step": int(nbytes[1]),
+           "workload": f"{args.e2e_gib:g} GiB coded packet of the same code/channel in pinned host memory"
+                       + (f", sharded over {world} ranks (each rank's shard in its own pinned buffer, all ranks "
+                          f"concurrently; bytes are the sum over ranks)" if world > 1 else "")
+                       + f", hamming_decode_host (chunk {chunk} codewords, 3 streams), wall clock per call, "
+                         f"max over ranks (measured, not extrapolated)",
            "steps": steps, "ms_per_step": round(t * 1e3, 2)}
     del rx_h, data_h, syn_h, ws
     return out

@@ -126,7 +126,12 @@ hamming_status hamming_channel_generate(int m, uint64_t seed, uint64_t c_first,
  *   host memory (pinned memory gives full PCIe bandwidth; pageable works).
  *   corrected_host: host uint64, overwritten.
  *   workspace_dev: device memory of hamming_host_workspace_bytes(m,
- *   chunk_codewords, n_streams, syndromes_host != NULL) bytes, 16-byte aligned.
+ *   chunk_codewords, n_streams, syndromes_host != NULL) bytes, 16-byte aligned,
+ *   on the current device; the C ABI cannot check its size (the Python
+ *   binding does).  The library's streams (created once per thread and device,
+ *   reused) do not wait on any caller stream: the caller must have completed
+ *   all work that touches the workspace (the binding synchronises its current
+ *   stream first).
  * Synchronous: returns when all outputs are in host memory. */
 size_t hamming_host_workspace_bytes(int m, uint64_t chunk_codewords, int n_streams,
                                     int with_syndromes);
@@ -172,7 +177,9 @@ hamming_status hamming_channel_generate_secded(int m, uint64_t seed, uint64_t c_
  * and the minimal r_i with 2^r >= k + r + 1, n_i = k_i + r_i.  The
  * encoded packet is H_1 ... H_t concatenated bitwise, LSB-first.  Packet j
  * starts at byte j*rx_stride (rx_stride a multiple of 16, >= the coded bytes
- * rounded up to 16); its message at byte j*msg_stride. */
+ * rounded up to 16; for hamming_decode_packets also <= 100 KiB, since the
+ * decoder stages whole strides in shared memory); its message at byte j*msg_stride.  HAMMING_E_ARG for a bad stride,
+ * HAMMING_E_RANGE if n_packets * stride overflows. */
 uint64_t hamming_packet_coded_bytes(uint32_t msg_bytes, int t); /* 0 on bad arguments */
 hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t *seg_k_host, uint32_t *seg_n_host);
 
@@ -182,7 +189,10 @@ hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t *seg_k_
  *   syndromes_dev: n_packets*t uint16 or NULL; status_dev: n_packets bytes or
  *   NULL (0 clean, 1 corrected, 2 some segment uncorrectable); counts_dev: 2
  *   device uint64 or NULL, OVERWRITTEN with {segments corrected, segments
- *   uncorrectable}.  rx 16-byte aligned; buffers must not overlap. */
+ *   uncorrectable}.  rx 16-byte aligned, syndromes 2-byte aligned, counts
+ *   8-byte aligned (HAMMING_E_MISALIGNED); no two of rx, msg, syndromes,
+ *   status, counts may overlap (HAMMING_E_OVERLAP).  All checks return
+ *   before any launch. */
 hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void *rx_dev, uint64_t rx_stride,
                                       uint64_t n_packets, void *msg_dev, uint64_t msg_stride,
                                       uint16_t *syndromes_dev, uint8_t *status_dev,

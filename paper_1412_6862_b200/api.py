@@ -8,6 +8,7 @@ packed streams; codeword c = stream bits [c*n, c*n + n); data bits of c at
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 from typing import Optional
@@ -67,6 +68,31 @@ def _dev_ptr(t: Optional[torch.Tensor], name: str, min_bytes: int):
     return t.data_ptr()  # an int; the argtypes make it a void*
 
 
+def _device_of(*tensors):
+    """The one CUDA device all the given tensors (None skipped) live on."""
+    dev = None
+    for t in tensors:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("every device buffer must be a CUDA tensor")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"buffers on different devices: {dev} and {t.device}")
+    return dev
+
+
+def _on(dev):
+    """Make `dev` current for the duration of a C-ABI call: the library launches on
+    the current device, and the stream handle comes from `dev`.  No-op (no context
+    switch) in the common case that it already is."""
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if torch.cuda.current_device() == idx:
+        return contextlib.nullcontext()
+    return torch.cuda.device(idx)
+
+
 # torch's current raw cudaStream_t without building a Stream object (a few us per call on the
 # latency-bound small-packet path); the public API is the fallback
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -105,10 +131,12 @@ def hamming_decode(m: int, rx: torch.Tensor, n_codewords: int, *, data_out: Opti
         syn = syndromes
     if corrected is None:
         corrected = torch.empty(1, dtype=torch.int64, device=dev)
-    st = lib().hamming_decode(m, _dev_ptr(rx, "rx", coded_bytes(m, N)), N,
-                              _dev_ptr(data_out, "data_out", data_bytes(m, N)),
-                              _dev_ptr(syn, "syndromes", N), _dev_ptr(corrected, "corrected", 8),
-                              _stream_handle(stream, dev))
+    dev = _device_of(rx, data_out, syn, corrected)
+    with _on(dev):
+        st = lib().hamming_decode(m, _dev_ptr(rx, "rx", coded_bytes(m, N)), N,
+                                  _dev_ptr(data_out, "data_out", data_bytes(m, N)),
+                                  _dev_ptr(syn, "syndromes", N), _dev_ptr(corrected, "corrected", 8),
+                                  _stream_handle(stream, dev))
     check(st, "hamming_decode")
     return DecodeResult(data_out, syn, corrected)
 
@@ -122,8 +150,10 @@ def hamming_encode(m: int, data: torch.Tensor, n_codewords: int, *, rx_out: Opti
     N = int(n_codewords)
     if rx_out is None:
         rx_out = torch.empty(max(1, coded_bytes(m, N)), dtype=torch.uint8, device=data.device)
-    st = lib().hamming_encode(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
-                              _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)), _stream_handle(stream, data.device))
+    dev = _device_of(data, rx_out)
+    with _on(dev):
+        st = lib().hamming_encode(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
+                                  _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)), _stream_handle(stream, dev))
     check(st, "hamming_encode")
     return rx_out
 
@@ -141,9 +171,10 @@ def hamming_channel_generate(m: int, seed: int, c_first: int, n_codewords: int, 
     if rx_out is None:
         rx_out = torch.empty(max(1, coded_bytes(m, N)), dtype=torch.uint8,
                              device=device if device is not None else "cuda")
-    st = lib().hamming_channel_generate(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
-                                        _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)),
-                                        _stream_handle(stream, rx_out.device))
+    dev = _device_of(rx_out)
+    with _on(dev):
+        st = lib().hamming_channel_generate(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
+                                            _dev_ptr(rx_out, "rx_out", coded_bytes(m, N)), _stream_handle(stream, dev))
     check(st, "hamming_channel_generate")
     return rx_out
 
@@ -170,11 +201,19 @@ def hamming_decode_host(m: int, rx_host: torch.Tensor, n_codewords: int, data_ho
         raise ValueError("host buffers too small")
     if syndromes_host is not None and syndromes_host.numel() < N:
         raise ValueError("syndromes_host too small")
+    need = host_workspace_bytes(m, chunk_codewords, n_streams, syndromes_host is not None)
+    if need == 0:
+        raise ValueError("bad chunk_codewords / n_streams (1 <= n_streams <= 4)")
+    dev = _device_of(workspace)
     cnt = ctypes.c_ulonglong(0)
-    st = lib().hamming_decode_host(m, ctypes.c_void_p(rx_host.data_ptr()), N, ctypes.c_void_p(data_host.data_ptr()),
-                                   None if syndromes_host is None else ctypes.c_void_p(syndromes_host.data_ptr()),
-                                   ctypes.byref(cnt), _dev_ptr(workspace, "workspace", 1), chunk_codewords,
-                                   n_streams)
+    with _on(dev):
+        # the library's streams do not wait on torch's: finish whatever still uses the workspace
+        torch.cuda.current_stream(dev).synchronize()
+        st = lib().hamming_decode_host(m, ctypes.c_void_p(rx_host.data_ptr()), N,
+                                       ctypes.c_void_p(data_host.data_ptr()),
+                                       None if syndromes_host is None else ctypes.c_void_p(syndromes_host.data_ptr()),
+                                       ctypes.byref(cnt), _dev_ptr(workspace, "workspace", need), chunk_codewords,
+                                       n_streams)
     check(st, "hamming_decode_host")
     return int(cnt.value)
 
@@ -232,10 +271,12 @@ def hamming_decode_packets(msg_bytes: int, t: int, rx: torch.Tensor, n_packets: 
     syn = torch.empty((max(1, P), t), dtype=torch.int16, device=dev) if syndromes else None
     st = torch.empty(max(1, P), dtype=torch.uint8, device=dev) if status else None
     counts = torch.empty(2, dtype=torch.int64, device=dev)
-    rc = lib().hamming_decode_packets(msg_bytes, t, _dev_ptr(rx, "rx", rx_stride * P), rx_stride, P,
-                                      _dev_ptr(msg_out, "msg_out", msg_stride * P), msg_stride,
-                                      _dev_ptr(syn, "syndromes", 2 * t * P), _dev_ptr(st, "status", P),
-                                      _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
+    dev = _device_of(rx, msg_out, syn, st, counts)
+    with _on(dev):
+        rc = lib().hamming_decode_packets(msg_bytes, t, _dev_ptr(rx, "rx", rx_stride * P), rx_stride, P,
+                                          _dev_ptr(msg_out, "msg_out", msg_stride * P), msg_stride,
+                                          _dev_ptr(syn, "syndromes", 2 * t * P), _dev_ptr(st, "status", P),
+                                          _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
     check(rc, "hamming_decode_packets")
     return PacketDecodeResult(msg_out, syn, st, counts)
 
@@ -252,9 +293,11 @@ def hamming_encode_packets(msg_bytes: int, t: int, messages: torch.Tensor, n_pac
     P = int(n_packets)
     if rx_out is None:
         rx_out = torch.empty(max(1, P * rx_stride), dtype=torch.uint8, device=messages.device)
-    rc = lib().hamming_encode_packets(msg_bytes, t, _dev_ptr(messages, "messages", msg_stride * P), msg_stride, P,
-                                      _dev_ptr(rx_out, "rx_out", rx_stride * P), rx_stride,
-                                      _stream_handle(stream, messages.device))
+    dev = _device_of(messages, rx_out)
+    with _on(dev):
+        rc = lib().hamming_encode_packets(msg_bytes, t, _dev_ptr(messages, "messages", msg_stride * P), msg_stride,
+                                          P, _dev_ptr(rx_out, "rx_out", rx_stride * P), rx_stride,
+                                          _stream_handle(stream, dev))
     check(rc, "hamming_encode_packets")
     return rx_out
 
@@ -273,10 +316,12 @@ def hamming_packet_channel_generate(msg_bytes: int, t: int, seed: int, g_first: 
     device = device if device is not None else "cuda"
     rx = torch.empty(max(1, P * rx_stride), dtype=torch.uint8, device=device)
     msgs = torch.empty(max(1, P * msg_bytes), dtype=torch.uint8, device=device) if want_messages else None
-    rc = lib().hamming_packet_channel_generate(msg_bytes, t, seed & (2 ** 64 - 1), g_first, P, thresh, all_,
-                                               _dev_ptr(rx, "rx", rx_stride * P), rx_stride,
-                                               _dev_ptr(msgs, "messages", msg_bytes * P),
-                                               _stream_handle(stream, rx.device))
+    dev = _device_of(rx, msgs)
+    with _on(dev):
+        rc = lib().hamming_packet_channel_generate(msg_bytes, t, seed & (2 ** 64 - 1), g_first, P, thresh, all_,
+                                                   _dev_ptr(rx, "rx", rx_stride * P), rx_stride,
+                                                   _dev_ptr(msgs, "messages", msg_bytes * P),
+                                                   _stream_handle(stream, dev))
     check(rc, "hamming_packet_channel_generate")
     return rx, msgs
 
@@ -314,9 +359,11 @@ def hamming_decode_secded(m: int, rx: torch.Tensor, n_codewords: int, *, data_ou
         fl = flags
     if counts is None:
         counts = torch.empty(2, dtype=torch.int64, device=dev)
-    st = lib().hamming_decode_secded(m, _dev_ptr(rx, "rx", secded_coded_bytes(m, N)), N,
-                                     _dev_ptr(data_out, "data_out", data_bytes(m, N)), _dev_ptr(fl, "flags", N),
-                                     _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
+    dev = _device_of(rx, data_out, fl, counts)
+    with _on(dev):
+        st = lib().hamming_decode_secded(m, _dev_ptr(rx, "rx", secded_coded_bytes(m, N)), N,
+                                         _dev_ptr(data_out, "data_out", data_bytes(m, N)), _dev_ptr(fl, "flags", N),
+                                         _dev_ptr(counts, "counts", 16), _stream_handle(stream, dev))
     check(st, "hamming_decode_secded")
     return SecdedResult(data_out, fl, counts)
 
@@ -329,9 +376,11 @@ def hamming_encode_secded(m: int, data: torch.Tensor, n_codewords: int, *, rx_ou
     N = int(n_codewords)
     if rx_out is None:
         rx_out = torch.empty(max(1, secded_coded_bytes(m, N)), dtype=torch.uint8, device=data.device)
-    st = lib().hamming_encode_secded(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
-                                     _dev_ptr(rx_out, "rx_out", secded_coded_bytes(m, N)),
-                                     _stream_handle(stream, data.device))
+    dev = _device_of(data, rx_out)
+    with _on(dev):
+        st = lib().hamming_encode_secded(m, _dev_ptr(data, "data", data_bytes(m, N)), N,
+                                         _dev_ptr(rx_out, "rx_out", secded_coded_bytes(m, N)),
+                                         _stream_handle(stream, dev))
     check(st, "hamming_encode_secded")
     return rx_out
 
@@ -346,9 +395,11 @@ def hamming_channel_generate_secded(m: int, seed: int, c_first: int, n_codewords
     thresh, all_, q2t = channel_thresholds(p, q2)
     rx = torch.empty(max(1, secded_coded_bytes(m, N)), dtype=torch.uint8,
                      device=device if device is not None else "cuda")
-    st = lib().hamming_channel_generate_secded(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
-                                               _dev_ptr(rx, "rx", secded_coded_bytes(m, N)),
-                                               _stream_handle(stream, rx.device))
+    dev = _device_of(rx)
+    with _on(dev):
+        st = lib().hamming_channel_generate_secded(m, seed & (2 ** 64 - 1), c_first, N, thresh, all_, q2t,
+                                                   _dev_ptr(rx, "rx", secded_coded_bytes(m, N)),
+                                                   _stream_handle(stream, dev))
     check(st, "hamming_channel_generate_secded")
     return rx
 

@@ -47,7 +47,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <type_traits>
 
 #include "hamming.h"
@@ -1491,6 +1494,48 @@ int sm_count(int dev) {
   return v;
 }
 
+// One-time kernel attribute setup per (kernel, device) -- the dynamic shared
+// memory limit raised to the 227 KB maximum, optionally the full carveout --
+// and memoised occupancy per (kernel, device, block size, shared memory), so
+// a warm call makes no attribute or occupancy query (latency-bound small
+// packet calls of the packet / long-code launchers).
+struct OccKey {
+  const void* fn;
+  int dev, threads;
+  size_t smem;
+  bool operator<(const OccKey& o) const {
+    return std::tie(fn, dev, threads, smem) < std::tie(o.fn, o.dev, o.threads, o.smem);
+  }
+};
+std::mutex g_occ_mu;
+std::map<OccKey, int> g_occ;
+std::set<std::pair<const void*, int>> g_attr_done;
+
+hamming_status kernel_blocks_per_sm(const void* fn, int dev, int threads, size_t smem, bool carveout, int& occ) {
+  std::lock_guard<std::mutex> lock(g_occ_mu);
+  const OccKey key{fn, dev, threads, smem};
+  const auto it = g_occ.find(key);
+  if (it != g_occ.end()) {
+    occ = it->second;
+    return HAMMING_OK;
+  }
+  if (g_attr_done.count({fn, dev}) == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(max dynamic shared memory)");
+    if (carveout) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+    }
+    g_attr_done.insert({fn, dev});
+  }
+  int v = 0;
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  occ = std::max(1, v);
+  g_occ[key] = occ;
+  return HAMMING_OK;
+}
+
 template <class Op, int WARPS, int STAGES, bool INPLACE = true>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
@@ -1680,24 +1725,33 @@ bool bits_overflow(int m, uint64_t N) {
 // Below this many codewords a call uses the light small-packet launch.
 constexpr uint64_t kSmallPacketCw = 1u << 16;
 
-// One-time per-device build of the (15,11) table in global memory.
-std::once_flag g_lut15_once[kMaxDev];
-cudaError_t g_lut15_err[kMaxDev];
+// Per-device build of the (15,11) table in global memory, once it succeeds: a
+// failed build (e.g. a first call made while the caller's stream is being
+// captured into a CUDA graph, where the build's own stream sync is not
+// allowed) is reported and retried by the next call, never latched.
+std::mutex g_lut15_mu;
+std::atomic<bool> g_lut15_ok[kMaxDev];
 
-hamming_status ensure_lut15(int dev) {
+hamming_status ensure_lut15(int dev, cudaStream_t caller) {
   if (dev < 0 || dev >= kMaxDev) return set_err(HAMMING_E_CUDA, "device index out of range");
-  std::call_once(g_lut15_once[dev], [dev] {
-    cudaStream_t s = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    if (e == cudaSuccess) {
-      init_lut15_kernel<<<32768 / 256, 256, 0, s>>>();
-      e = cudaGetLastError();
-      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    }
-    g_lut15_err[dev] = e;
-  });
-  if (g_lut15_err[dev] != cudaSuccess) return cuda_fail(g_lut15_err[dev], "building the (15,11) table");
+  if (g_lut15_ok[dev].load(std::memory_order_acquire)) return HAMMING_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(caller, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return set_err(HAMMING_E_CUDA,
+                   "the (15,11)/(31,26) lookup table is built by the first eager call on a device; "
+                   "make one call outside CUDA-graph capture first");
+  std::lock_guard<std::mutex> lock(g_lut15_mu);
+  if (g_lut15_ok[dev].load(std::memory_order_acquire)) return HAMMING_OK;
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    init_lut15_kernel<<<32768 / 256, 256, 0, s>>>();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "building the (15,11) table");
+  g_lut15_ok[dev].store(true, std::memory_order_release);
   return HAMMING_OK;
 }
 
@@ -1740,7 +1794,7 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       int dev = 0;
       const cudaError_t e = cudaGetDevice(&dev);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-      const hamming_status rc = ensure_lut15(dev);
+      const hamming_status rc = ensure_lut15(dev, st);
       if (rc != HAMMING_OK) return rc;
       return Launcher<DecodeLut4Op, HAM_W4, HAM_S4, HAM_IP4>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                   accumulate);
@@ -1749,7 +1803,7 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       int dev = 0;
       const cudaError_t e = cudaGetDevice(&dev);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-      const hamming_status rc = ensure_lut15(dev);
+      const hamming_status rc = ensure_lut15(dev, st);
       if (rc != HAMMING_OK) return rc;
       return Launcher<DecodeLut5Op, HAM_W5, HAM_S5, HAM_IP5>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                   accumulate);
@@ -1949,14 +2003,28 @@ hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void*
   const HostSlotLayout L = host_slot_layout(m, chunk, syn_host != nullptr);
   uint8_t* ws = static_cast<uint8_t*>(workspace_dev);
   unsigned long long* total = reinterpret_cast<unsigned long long*>(ws);
-  cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t ready = nullptr;
+  // the pipeline's streams and event: created once per (thread, device) and reused, so a
+  // call makes no stream / event create or destroy (never destroyed: they live as long as
+  // the thread, and tearing them down at thread exit could race the runtime's own exit)
+  struct HostPipe {
+    cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ready = nullptr;
+  };
+  static thread_local HostPipe pipes[kMaxDev];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= kMaxDev) return set_err(HAMMING_E_CUDA, "device index out of range");
+  HostPipe& P = pipes[dev];
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+    if (P.s[i] == nullptr) e = cudaStreamCreateWithFlags(&P.s[i], cudaStreamNonBlocking);
+  if (e == cudaSuccess && P.ready == nullptr) e = cudaEventCreateWithFlags(&P.ready, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "hamming_decode_host: stream setup");
+  cudaStream_t* streams = P.s;
+  cudaEvent_t ready = P.ready;
   hamming_status rc = HAMMING_OK;
-  cudaError_t e = cudaSuccess;
   int launches = 0;
-  for (int i = 0; i < n_streams && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&streams[i], cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaMemsetAsync(total, 0, sizeof(unsigned long long), streams[0]);
+  e = cudaMemsetAsync(total, 0, sizeof(unsigned long long), streams[0]);
   if (e == cudaSuccess) e = cudaEventRecord(ready, streams[0]);
   for (int i = 1; i < n_streams && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(streams[i], ready, 0);
   if (e != cudaSuccess) rc = cuda_fail(e, "hamming_decode_host setup");
@@ -1989,9 +2057,6 @@ hamming_status hamming_decode_host(int m, const void* rx_host, uint64_t N, void*
     e = cudaMemcpy(corrected_host, total, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = cuda_fail(e, "hamming_decode_host count D2H");
   }
-  if (ready) cudaEventDestroy(ready);
-  for (int i = 0; i < n_streams; ++i)
-    if (streams[i]) cudaStreamDestroy(streams[i]);
   g_launches = launches;
   return rc;
 }
@@ -2042,7 +2107,7 @@ hamming_status hamming_decode_secded(int m, const void* rx_dev, uint64_t N, void
     int dev = 0;
     const cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    const hamming_status rc = ensure_lut15(dev);
+    const hamming_status rc = ensure_lut15(dev, st);
     if (rc != HAMMING_OK) return rc;
   }
   if (N < kSmallPacketCw) {
@@ -2156,8 +2221,21 @@ hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void* rx_
   if (n_packets > 0 && (rx_dev == nullptr || msg_dev == nullptr))
     return set_err(HAMMING_E_NULL, "hamming_decode_packets: NULL buffer");
   if (msg_stride < msg_bytes) return set_err(HAMMING_E_ARG, "hamming_decode_packets: msg_stride < msg_bytes");
-  if (n_packets > 0 && ranges_overlap(rx_dev, rx_stride * n_packets, msg_dev, msg_stride * n_packets))
-    return set_err(HAMMING_E_OVERLAP, "hamming_decode_packets: buffers overlap");
+  if (n_packets > (~0ull) / rx_stride || n_packets > (~0ull) / msg_stride ||
+      n_packets > (~0ull) / (2ull * static_cast<uint64_t>(t)))
+    return set_err(HAMMING_E_RANGE, "hamming_decode_packets: n_packets * stride overflows");
+  if ((reinterpret_cast<uintptr_t>(syndromes_dev) & 1u) != 0 || (reinterpret_cast<uintptr_t>(counts_dev) & 7u) != 0)
+    return set_err(HAMMING_E_MISALIGNED,
+                   "hamming_decode_packets: syndromes must be 2-byte and counts 8-byte aligned");
+  {
+    const void* buf[5] = {rx_dev, msg_dev, syndromes_dev, status_dev, counts_dev};
+    const uint64_t len[5] = {rx_stride * n_packets, msg_stride * n_packets, 2ull * t * n_packets, n_packets,
+                             counts_dev ? 16u : 0u};
+    for (int i = 0; i < 5; ++i)
+      for (int j = i + 1; j < 5; ++j)
+        if (ranges_overlap(buf[i], len[i], buf[j], len[j]))
+          return set_err(HAMMING_E_OVERLAP, "hamming_decode_packets: buffers overlap");
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (counts_dev != nullptr) {
     const cudaError_t e = cudaMemsetAsync(counts_dev, 0, 2 * sizeof(unsigned long long), st);
@@ -2185,6 +2263,10 @@ hamming_status hamming_encode_packets(uint32_t msg_bytes, int t, const void* msg
   if (n_packets > 0 && (rx_dev == nullptr || msg_dev == nullptr))
     return set_err(HAMMING_E_NULL, "hamming_encode_packets: NULL buffer");
   if (msg_stride < msg_bytes) return set_err(HAMMING_E_ARG, "hamming_encode_packets: msg_stride < msg_bytes");
+  if (n_packets > (~0ull) / rx_stride || n_packets > (~0ull) / msg_stride)
+    return set_err(HAMMING_E_RANGE, "hamming_encode_packets: n_packets * stride overflows");
+  if (n_packets > 0 && ranges_overlap(msg_dev, msg_stride * n_packets, rx_dev, rx_stride * n_packets))
+    return set_err(HAMMING_E_OVERLAP, "hamming_encode_packets: buffers overlap");
   PacketArgs a{};
   a.in = static_cast<const uint8_t*>(msg_dev);
   a.in_stride = msg_stride;
@@ -2203,6 +2285,8 @@ hamming_status hamming_packet_channel_generate(uint32_t msg_bytes, int t, uint64
   hamming_status rc = packet_common(msg_bytes, t, rx_stride, rx_dev, g, "hamming_packet_channel_generate");
   if (rc != HAMMING_OK) return rc;
   if (n_packets > 0 && rx_dev == nullptr) return set_err(HAMMING_E_NULL, "hamming_packet_channel_generate: NULL rx");
+  if (n_packets > (~0ull) / rx_stride || n_packets > (~0ull) / msg_bytes)
+    return set_err(HAMMING_E_RANGE, "hamming_packet_channel_generate: n_packets * stride overflows");
   PacketArgs a{};
   a.out = static_cast<uint8_t*>(rx_dev);
   a.out_stride = rx_stride;

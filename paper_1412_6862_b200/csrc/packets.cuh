@@ -229,11 +229,10 @@ hamming_status launch_packets(const PacketGeom& g, const PacketArgs& a, cudaStre
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   const size_t smem = static_cast<size_t>(kPktWarps) * (g.in_cap + g.msg_cap);
   auto kfn = packets_kernel<MODE>;
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets)");
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kPktWarps * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets)");
+  const hamming_status rc = kernel_blocks_per_sm(reinterpret_cast<const void*>(kfn), dev, kPktWarps * 32, smem,
+                                                 false, occ);
+  if (rc != HAMMING_OK) return rc;
   const uint64_t want = (a.n_packets + kPktWarps - 1) / kPktWarps;
   const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
   if (grid > 0) {
@@ -407,6 +406,9 @@ struct BatchGeom {
 };
 
 hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
+  // a warp stages kPktStages whole strides: larger strides cannot be staged
+  if (stride > (200u << 10) / kPktStages)
+    return set_err(HAMMING_E_ARG, "packets: rx_stride too large to stage in shared memory (max 100 KiB)");
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
   // Launch shape, measured (tools/tune_shapes.py packets): the trade is warps per SM
@@ -478,8 +480,12 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
                  static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
   b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
-  if (b.tab_bytes + b.warp_bytes * 2ull > 227ull * 1024)
-    return set_err(HAMMING_E_ARG, "packets: batch does not fit shared memory");
+  // a padded stride (any multiple of 16 >= the coded bytes is legal) can make the
+  // shape's warps overflow shared memory: fewer warps per CTA then (the kernel
+  // takes its warp count from blockDim)
+  while (b.warps > 1 && b.tab_bytes + static_cast<uint64_t>(b.warps) * b.warp_bytes > 227ull * 1024) --b.warps;
+  if (b.tab_bytes + static_cast<uint64_t>(b.warp_bytes) > 227ull * 1024)
+    return set_err(HAMMING_E_ARG, "packets: one packet (rx_stride) does not fit shared memory");
   return HAMMING_OK;
 }
 
@@ -845,14 +851,10 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
     HAM_PKT_KFN(false)
   }
 #undef HAM_PKT_KFN
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(packets decode)");
-  // ask for the full shared-memory carveout so several CTAs fit per SM
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
+  // the full shared-memory carveout so several CTAs fit per SM
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, bg.warps * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "occupancy(packets decode)");
+  rc = kernel_blocks_per_sm(reinterpret_cast<const void*>(kfn), dev, bg.warps * 32, smem, true, occ);
+  if (rc != HAMMING_OK) return rc;
   const uint64_t batches = (a.n_packets + bg.G - 1) / bg.G;
   const uint64_t want = (batches + bg.warps - 1) / bg.warps;
   const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
@@ -1094,13 +1096,9 @@ hamming_status launch_perfect_long(const LongArgs& a0, cudaStream_t st, bool acc
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   auto kfn = perfect_long_kernel<M, WARPS>;
   const size_t smem = static_cast<size_t>(WARPS) * (2 * G::IN_BYTES + G::OUT_BYTES);
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(long decode)");
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(carveout)");
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, WARPS * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "occupancy(long decode)");
+  const hamming_status rc = kernel_blocks_per_sm(reinterpret_cast<const void*>(kfn), dev, WARPS * 32, smem, true, occ);
+  if (rc != HAMMING_OK) return rc;
   const uint64_t batches = (a.N + G::B - 1) / G::B;
   const uint64_t want = (batches + WARPS - 1) / WARPS;
   const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));

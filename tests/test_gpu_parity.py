@@ -3,6 +3,8 @@ bit for bit, on identical seeded packets -- data stream, syndromes and the
 corrected count -- including multi-error codewords (where both must make the
 same miscorrection), ragged tails, empty input and every received word of
 the (7,4) and (15,11) codes."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -11,6 +13,7 @@ import paper_1412_6862_b200 as ham
 
 pytestmark = pytest.mark.gpu
 
+THREADS = max(1, len(os.sched_getaffinity(0)))
 SIZES = [1, 31, 32, 33, 127, 128, 129, 1023, 1024, 1025, 4681, 3 * 1024 + 17, 7 * 1024, 50_000]
 
 
@@ -64,6 +67,35 @@ def test_every_received_word(oracle, m, N):
     bits = ((words[:, None] >> np.arange(n)) & 1).astype(np.uint8).reshape(-1)
     rx = np.packbits(bits, bitorder="little")
     assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
+
+
+@pytest.mark.parametrize("m", [2, 3, 4])
+def test_every_received_word_tiled_large(oracle, m):
+    """Every received word of the code at N >= 2^17 codewords (a ragged tail
+    included), i.e. through the multi-CTA launches that serve every call of
+    >= 65 536 codewords -- the (7,4) / (15,11) table decoders for m = 3, 4.
+    Each block of 2^n words is a fresh permutation, so every word lands on
+    many codeword slots of a lane."""
+    n = 2 ** m - 1
+    rng = np.random.default_rng(1000 + m)
+    blocks = max(1, ((1 << 17) + 2 ** n - 1) // 2 ** n) + 1
+    words = np.concatenate([rng.permutation(2 ** n) for _ in range(blocks)]).astype(np.int64)
+    N = (1 << 17) + 77 if m < 4 else words.size - 1234
+    words = words[:N]
+    bits = ((words[:, None] >> np.arange(n)) & 1).astype(np.uint8).reshape(-1)
+    rx = np.packbits(bits, bitorder="little")
+    assert_same(m, N, gpu_decode(m, rx, N), oracle.decode_mt(m, rx, N, THREADS))
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("N", [65535, 65536, 65537, 10 ** 6 + 13])
+def test_uniform_random_streams_large(oracle, m, N):
+    """Uniformly random received bits (nearly every codeword erroneous, many
+    with several flips) with garbage in the input pad bits, on both sides of
+    the small-packet launch threshold and at 10^6 + 13 codewords."""
+    rng = np.random.default_rng(m * 7919 + N)
+    rx = rng.integers(0, 256, ham.coded_bytes(m, N), dtype=np.uint8)
+    assert_same(m, N, gpu_decode(m, rx, N), oracle.decode_mt(m, rx, N, THREADS))
 
 
 @pytest.mark.parametrize("m", [3, 5, 6])

@@ -74,3 +74,16 @@ def test_secded_large_counts(oracle, m):
     k = 2 ** m - 1 - m
     assert np.array_equal(res.data[c0 * k // 8: c0 * k // 8 + wd.size - 1].cpu().numpy(), wd[:-1])
     assert np.array_equal(f[c0: c0 + w].cpu().numpy(), wf)
+
+
+@pytest.mark.parametrize("m", [3, 4, 5, 6])
+@pytest.mark.parametrize("N", [65535, 65536, 65537, 10 ** 6 + 13])
+def test_uniform_random_streams_large(oracle, m, N):
+    """Uniformly random SECDED words (single, double and heavier errors in
+    every mix) through the multi-CTA table / POPC decoders (>= 65 536
+    codewords) and the small launch just below."""
+    rng = np.random.default_rng(m * 131 + N)
+    rx = rng.integers(0, 256, ham.secded_coded_bytes(m, N), dtype=np.uint8)
+    wd, wf, c1, c2 = oracle.decode_secded(m, rx, N)
+    d, f, c = gpu_decode(m, rx, N)
+    assert np.array_equal(d, wd) and np.array_equal(f, wf) and c == [c1, c2]
