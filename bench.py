@@ -477,7 +477,8 @@ def _median(xs):
 
 def run_sweeps(ham, torch, dev, peak):
     """BASELINE.json's other configs, timed in the same run on the same GPU
-    (device time, CUDA events on the launching stream):
+    (device time, CUDA events on the launching stream), starting from an idle
+    GPU (a 3 s pause after the sustained C5 run, 0.5 s between C3 points):
       c3: 256 MiB per call, every m, with and without syndromes -- median of
           20 back-to-back calls alternating between two buffer sets (cold by
           size: 0.55-0.73 GB moved per call vs a 126 MB L2);
@@ -493,6 +494,13 @@ def run_sweeps(ham, torch, dev, peak):
     st = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     out = {"method": run_sweeps.__doc__.split("\n", 1)[1].strip()}
+    # the sweeps are per-call (burst) rates: start them from an idle GPU, not from the
+    # board power cap the sustained C5 run leaves behind (it takes ~1 s to lift), and
+    # record what the clocks did meanwhile
+    torch.cuda.synchronize()
+    time.sleep(3.0)
+    sampler = ClockSampler(dev.index)
+    sampler.start()
 
     def alg(m, N, syn=True):
         return ham.coded_bytes(m, N) + ham.data_bytes(m, N) + (N if syn else 0) + 8
@@ -525,6 +533,7 @@ def run_sweeps(ham, torch, dev, peak):
             row["frac" + key] = round(alg(m, N, syn_on) / t / 1e9 / peak, 4)
         pts.append(row)
         del sets
+        time.sleep(0.5)
     out["c3_code_length_256MiB"] = {"unit": "coded Gbit/s", "peak_gbs": peak, "points": pts}
     torch.cuda.empty_cache()
 
@@ -639,6 +648,7 @@ def run_sweeps(ham, torch, dev, peak):
                          "note": "graph: 1000 distinct packets per replay, L2-resident (warm)"}
     del flush, big, bd, bs, bc, g
     torch.cuda.empty_cache()
+    out["clocks"] = sampler.stop()
     return out
 
 

@@ -1335,15 +1335,33 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define HAM_STAMP(i)
 #endif
 
+// Per-launch scratch for the count and the dynamic tail, one per (device,
+// stream) (host map below; never shared by two launches that can run at the
+// same time): every CTA adds its partial count to `sum`, and the LAST CTA to
+// arrive at `done` writes the total into the caller's count (overwrite, or add
+// in accumulate mode) and resets the slot to zero for the stream's next
+// launch -- so a call needs no cudaMemsetAsync of the count before its kernel.
+// `claim` hands out the dynamically scheduled tail tiles.
+struct LaunchSlot {
+  unsigned long long sum[2];
+  unsigned int claim;
+  unsigned int done;
+};
+constexpr int kSlots = 256;
+__device__ LaunchSlot g_slots[kSlots];  // zero-initialised at module load
+
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
 template <class Op, int WARPS, int STAGES, bool INPLACE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     tiles_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ side,
                  uint64_t n_full, uint32_t rem, uint64_t in_total, uint64_t out_total,
-                 unsigned long long* __restrict__ counter, int store_count,
-                 const __grid_constant__ typename Op::Args args) {
+                 unsigned long long* __restrict__ counter, int store_count, LaunchSlot* __restrict__ slot,
+                 uint64_t static_end, int accumulate, const __grid_constant__ typename Op::Args args) {
   using TL = TileLayout<Op, INPLACE>;
   constexpr int IN = TL::IN, OUT = TL::OUT;
   constexpr int WARP_SMEM = TL::warp_bytes(STAGES);
+  static_assert(STAGES <= 32, "stage tile ids live one per lane");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long block_cnt[2];
 
@@ -1363,30 +1381,68 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const uint64_t gw = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
   const uint64_t pol = policy_evict_first();
+  // Schedule: tiles [0, static_end) round-robin (warp gw takes gw, gw + nw, ...:
+  // rs = static_end / nw of them each, no communication); tiles [static_end,
+  // n_full] -- n_full itself being the ragged tail when rem > 0 -- claimed one at
+  // a time from slot->claim, so the last rounds balance across warps and SMs.
+  // Without a dynamic part (static_end == n_full) the warp next in line takes
+  // the tail, as before.
+  const bool dyn = static_end < n_full;
+  const uint64_t rs = dyn ? static_end / nw : ~0ull;
+  bool exhausted = false, do_tail = false;
+  // tile of this warp's j-th sequence slot; claims are made by lane 0 in sequence
+  // order (every lane calls this, uniformly)
+  auto seq_tile = [&](uint64_t j) -> uint32_t {
+    if (!dyn) {
+      const uint64_t t = gw + j * nw;
+      return t < n_full ? static_cast<uint32_t>(t) : kNoTile;
+    }
+    if (j < rs) return static_cast<uint32_t>(gw + j * nw);
+    if (exhausted) return kNoTile;
+    uint32_t d = 0;
+    if (lane == 0) d = atomicAdd(&slot->claim, 1u);
+    d = __shfl_sync(0xffffffffu, d, 0);
+    const uint64_t t = static_end + d;
+    if (t >= n_full) {  // the ragged tail (t == n_full, rem > 0) or nothing: no more tiles
+      exhausted = true;
+      if (t == n_full && rem > 0) do_tail = true;
+      return kNoTile;
+    }
+    return static_cast<uint32_t>(t);
+  };
 
   if (threadIdx.x < 2) block_cnt[threadIdx.x] = 0;
   if constexpr (Op::SHARED > 0) {
     Op::cta_init(sh, threadIdx.x, blockDim.x);
     __syncthreads();
   }
+  uint32_t stage_tile = kNoTile;  // lane s: the tile in stage s
   if constexpr (IN > 0) {
     if (lane == 0) {
 #pragma unroll
       for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
       fence_mbar_init();
+    }
 #pragma unroll
-      for (int s = 0; s < STAGES; ++s) {
-        const uint64_t t = gw + s * nw;
-        if (t < n_full) load_tile<Op>(wbase + s * IN, in, t, &bars[s], args, pol);
-      }
+    for (int s = 0; s < STAGES; ++s) {
+      const uint32_t t = seq_tile(s);
+      if (lane == s) stage_tile = t;
+      if (lane == 0 && t != kNoTile) load_tile<Op>(wbase + s * IN, in, t, &bars[s], args, pol);
     }
     __syncwarp();
   }
 
   uint32_t cnt = 0, cnt2 = 0;
-  uint32_t it = 0;
-  for (uint64_t t = gw; t < n_full; t += nw, ++it) {
+  for (uint32_t it = 0;; ++it) {
     const int st = static_cast<int>(it % STAGES);
+    uint64_t t;
+    if constexpr (IN > 0) {
+      t = (it < rs) ? gw + static_cast<uint64_t>(it) * nw : __shfl_sync(0xffffffffu, stage_tile, st);
+      if (t >= n_full) break;  // kNoTile, or past the full tiles (static schedule)
+    } else {
+      t = gw + static_cast<uint64_t>(it) * nw;  // no input: a plain grid-stride walk
+      if (t >= n_full) break;
+    }
     uint32_t* obuf;
     if constexpr (TL::IN_PLACE) {
       mbar_wait(&bars[st], (it / STAGES) & 1u);
@@ -1414,21 +1470,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         bulk_s2g(out + t * OUT, obuf, OUT, pol);
       }
       bulk_commit();
-      if constexpr (TL::IN_PLACE) {
-        // refill the stage of the PREVIOUS tile: its in-place store was issued a
-        // whole tile ago, so waiting for it to have read shared memory is free
-        if (it > 0) {
-          const uint64_t nt = t - nw + STAGES * nw;
-          if (nt < n_full) {
-            const int ps = static_cast<int>((it - 1) % STAGES);
-            bulk_wait_read<1>();
-            load_tile<Op>(wbase + ps * IN, in, nt, &bars[ps], args, pol);
-          }
+    }
+    // the tile to prefetch: IN_PLACE refills the stage of the PREVIOUS tile (its in-place
+    // store was issued a whole tile ago, so waiting for it to have read shared memory is
+    // free); otherwise this tile's stage, whose input the lane function has consumed
+    if constexpr (IN > 0) {
+      if (!TL::IN_PLACE || it > 0) {
+        const int ps = TL::IN_PLACE ? static_cast<int>((it - 1) % STAGES) : st;
+        const uint32_t nt = seq_tile(static_cast<uint64_t>(it) + STAGES - (TL::IN_PLACE ? 1 : 0));
+        if (lane == ps) stage_tile = nt;
+        if (lane == 0 && nt != kNoTile) {
+          if constexpr (TL::IN_PLACE) bulk_wait_read<1>();
+          load_tile<Op>(wbase + ps * IN, in, nt, &bars[ps], args, pol);
         }
-      }
-      if constexpr (!TL::IN_PLACE && IN > 0) {
-        const uint64_t nt = t + STAGES * nw;
-        if (nt < n_full) load_tile<Op>(wbase + st * IN, in, nt, &bars[st], args, pol);
       }
     }
     if constexpr (Op::HAS_SIDE) {
@@ -1441,7 +1495,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if constexpr (Op::NCOUNT > 1) cnt2 += Op::count1(sidew);
     }
   }
-  if (rem > 0 && gw == n_full % nw) {  // the ragged tail tile
+  if (rem > 0 && (dyn ? do_tail : gw == n_full % nw)) {  // the ragged tail tile
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
     uint8_t* tail_out = TL::IN_PLACE ? wbase : wbase + TL::out_off(STAGES);
@@ -1452,7 +1506,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   if (lane == 0) bulk_wait<0>();
   HAM_STAMP(3);
 
-  if (counter != nullptr) {
+  if (counter != nullptr || slot != nullptr) {
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if constexpr (Op::NCOUNT > 1) cnt2 = __reduce_add_sync(0xffffffffu, cnt2);
     __syncthreads();
@@ -1460,7 +1514,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if constexpr (Op::NCOUNT > 1)
       if (lane == 0 && cnt2) atomicAdd(&block_cnt[1], static_cast<unsigned long long>(cnt2));
     __syncthreads();
-    if (threadIdx.x < Op::NCOUNT) {
+    if (slot != nullptr) {
+      if (threadIdx.x == 0) {
+        // the last CTA to arrive publishes the total and resets the slot (threadFence reduction)
+        for (int i = 0; i < Op::NCOUNT; ++i)
+          if (block_cnt[i]) atomicAdd(&slot->sum[i], block_cnt[i]);
+        __threadfence();
+        if (atomicAdd(&slot->done, 1u) == gridDim.x - 1) {
+          __threadfence();
+          for (int i = 0; i < Op::NCOUNT; ++i) {
+            const unsigned long long tot = atomicExch(&slot->sum[i], 0ull);
+            if (counter != nullptr) {
+              if (accumulate) atomicAdd(&counter[i], tot);
+              else counter[i] = tot;
+            }
+          }
+          slot->claim = 0;
+          slot->done = 0;
+        }
+      }
+    } else if (threadIdx.x < Op::NCOUNT) {
       const unsigned long long v = block_cnt[threadIdx.x];
       if (store_count) counter[threadIdx.x] = v;  // a single-CTA launch owns the count: no memset needed
       else if (v) atomicAdd(&counter[threadIdx.x], v);
@@ -1520,7 +1593,14 @@ hamming_status kernel_blocks_per_sm(const void* fn, int dev, int threads, size_t
     return HAMMING_OK;
   }
   if (g_attr_done.count({fn, dev}) == 0) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // the opt-in maximum per block less the kernel's static shared memory
+    int optin = 0;
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel attributes");
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - static_cast<int>(fa.sharedSizeBytes));
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(max dynamic shared memory)");
     if (carveout) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1536,6 +1616,41 @@ hamming_status kernel_blocks_per_sm(const void* fn, int dev, int threads, size_t
   return HAMMING_OK;
 }
 
+// The launch slot of (device, stream): a stream's launches run one after
+// another, so they can share one slot; launches on different streams get
+// different slots.  nullptr (use the memset + atomics path) when the stream is
+// being captured into a CUDA graph -- a replay may run on another stream,
+// concurrently with eager launches on this one -- or when every slot is taken.
+std::mutex g_slot_mu;
+std::map<std::pair<int, cudaStream_t>, int> g_slot_of;
+int g_slots_used[kMaxDev];
+
+LaunchSlot* launch_slot(int dev, cudaStream_t st) {
+  if (dev < 0 || dev >= kMaxDev) return nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  static LaunchSlot* base[kMaxDev] = {};
+  std::lock_guard<std::mutex> lock(g_slot_mu);
+  if (base[dev] == nullptr) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_slots) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    base[dev] = static_cast<LaunchSlot*>(p);
+  }
+  const auto key = std::make_pair(dev, st);
+  auto it = g_slot_of.find(key);
+  if (it == g_slot_of.end()) {
+    if (g_slots_used[dev] >= kSlots) return nullptr;
+    it = g_slot_of.emplace(key, g_slots_used[dev]++).first;
+  }
+  return base[dev] + it->second;
+}
+
 template <class Op, int WARPS, int STAGES, bool INPLACE = true>
 struct Launcher {
   static constexpr int IN = TileBytes<Op>::IN, OUT = TileBytes<Op>::OUT;
@@ -1544,9 +1659,11 @@ struct Launcher {
                                  WARPS * STAGES * 8;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 
+  // dyn_rounds > 0: the last ~dyn_rounds rounds of tiles are claimed dynamically
+  // (decoders with few tiles per warp, where one round is several % of the call)
   static hamming_status run(const uint8_t* in, uint8_t* out, uint8_t* side, uint64_t n_cw, uint64_t in_total,
                             uint64_t out_total, unsigned long long* counter, const typename Op::Args& args,
-                            cudaStream_t stream, bool accumulate = false) {
+                            cudaStream_t stream, bool accumulate = false, int dyn_rounds = 0) {
     static std::atomic<int> configured[kMaxDev];
     static std::atomic<int> blocks_per_sm[kMaxDev];
     int dev = 0;
@@ -1579,13 +1696,22 @@ struct Launcher {
       grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * bps));
     }
     const int store_count = (counter != nullptr && !accumulate && grid == 1) ? 1 : 0;
-    if (counter != nullptr && !accumulate && !store_count) {  // the count is overwritten, stream-ordered
+    // the slot: the count without a memset (multi-CTA launches) and the dynamic tail
+    LaunchSlot* slot = nullptr;
+    if (grid > 1 && (counter != nullptr || dyn_rounds > 0)) slot = launch_slot(dev, stream);
+    uint64_t static_end = n_full;
+    if (slot != nullptr && dyn_rounds > 0 && n_full < (1ull << 31)) {
+      const uint64_t nw = static_cast<uint64_t>(grid) * WARPS;
+      const uint64_t rounds = n_full / nw;
+      static_end = (rounds > static_cast<uint64_t>(dyn_rounds) ? rounds - dyn_rounds : 0) * nw;
+    }
+    if (counter != nullptr && !accumulate && !store_count && slot == nullptr) {  // overwritten, stream-ordered
       e = cudaMemsetAsync(counter, 0, Op::NCOUNT * sizeof(unsigned long long), stream);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
     }
     if (grid > 0) {
       kfn<<<grid, WARPS * 32, SMEM, stream>>>(in, out, side, n_full, rem, in_total, out_total, counter,
-                                              store_count, args);
+                                              store_count, slot, static_end, accumulate ? 1 : 0, args);
       ++launches;
       e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e, "tiles kernel launch");
@@ -1722,6 +1848,22 @@ bool bits_overflow(int m, uint64_t N) {
 #define HAM_IP6 true
 #endif
 
+// Rounds of tiles claimed dynamically at the end of a decode launch (0 = all
+// static); measured, tools/tune_shapes.py.  The claims go through one L2
+// atomic, so codes with many (short) tiles per warp keep the static schedule.
+#ifndef HAM_DYN3
+#define HAM_DYN3 0
+#endif
+#ifndef HAM_DYN4
+#define HAM_DYN4 0
+#endif
+#ifndef HAM_DYN5
+#define HAM_DYN5 2
+#endif
+#ifndef HAM_DYN6
+#define HAM_DYN6 2
+#endif
+
 // Below this many codewords a call uses the light small-packet launch.
 constexpr uint64_t kSmallPacketCw = 1u << 16;
 
@@ -1789,7 +1931,7 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
                                                                  accumulate);
     case 3:
       return Launcher<DecodeLut3Op, HAM_W3, HAM_S3, HAM_IP3>::run(in, out, syn, N, ib, ob, counter, {}, st,
-                                                                  accumulate);
+                                                                  accumulate, HAM_DYN3);
     case 4: {
       int dev = 0;
       const cudaError_t e = cudaGetDevice(&dev);
@@ -1797,7 +1939,7 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       const hamming_status rc = ensure_lut15(dev, st);
       if (rc != HAMMING_OK) return rc;
       return Launcher<DecodeLut4Op, HAM_W4, HAM_S4, HAM_IP4>::run(in, out, syn, N, ib, ob, counter, {}, st,
-                                                                  accumulate);
+                                                                  accumulate, HAM_DYN4);
     }
     case 5: {
       int dev = 0;
@@ -1806,11 +1948,11 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       const hamming_status rc = ensure_lut15(dev, st);
       if (rc != HAMMING_OK) return rc;
       return Launcher<DecodeLut5Op, HAM_W5, HAM_S5, HAM_IP5>::run(in, out, syn, N, ib, ob, counter, {}, st,
-                                                                  accumulate);
+                                                                  accumulate, HAM_DYN5);
     }
     case 6:
       return Launcher<DecodeOp<6>, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn, N, ib, ob, counter, {}, st,
-                                                                 accumulate);
+                                                                 accumulate, HAM_DYN6);
   }
   return set_err(HAMMING_E_INVALID_M, "decode: m must be in [2, 6]");
 }

@@ -907,7 +907,7 @@ struct LongGeo {
 
 template <int M>
 __device__ __forceinline__ uint32_t long_batch(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                               uint8_t* __restrict__ syn, uint32_t nvalid, uint32_t lane) {
+                                               uint8_t* __restrict__ sbuf, uint32_t nvalid, uint32_t lane) {
   using G = LongGeo<M>;
   constexpr int UW = G::UW, k = G::k, KW = G::KW;
   uint32_t cnt = 0;
@@ -993,10 +993,8 @@ __device__ __forceinline__ uint32_t long_batch(const uint32_t* __restrict__ in, 
 #pragma unroll
     for (int j = 0; j <= KW; ++j)
       if (static_cast<uint32_t>(j) < nw && !(static_cast<uint32_t>(j) + 1 == nw && end_partial)) ob[j] = O[j];
-    if (c < nvalid) {
-      if (syn != nullptr) syn[c] = static_cast<uint8_t>(s);
-      cnt += (s != 0);
-    }
+    sbuf[c] = static_cast<uint8_t>(s);  // staged: the batch's B syndrome bytes leave by one bulk store
+    cnt += (c < nvalid) & (s != 0);
   }
   return cnt;
 }
@@ -1005,8 +1003,8 @@ template <int M, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     perfect_long_kernel(const __grid_constant__ LongArgs a) {
   using G = LongGeo<M>;
-  constexpr uint32_t IN_B = G::IN_BYTES, OUT_B = G::OUT_BYTES;
-  constexpr uint32_t WARP_BYTES = 2 * IN_B + OUT_B;
+  constexpr uint32_t IN_B = G::IN_BYTES, OUT_B = G::OUT_BYTES, SYN_B = G::B;
+  constexpr uint32_t WARP_BYTES = 2 * IN_B + OUT_B + SYN_B;  // every part a multiple of 16 bytes
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_count;
   __shared__ __align__(8) uint64_t bars_all[WARPS * 2];
@@ -1014,6 +1012,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const uint32_t lane = threadIdx.x & 31u;
   uint8_t* wb = smem + warp * WARP_BYTES;
   uint32_t* obuf = reinterpret_cast<uint32_t*>(wb + 2 * IN_B);
+  uint8_t* sbuf = wb + 2 * IN_B + OUT_B;
   uint64_t* bars = bars_all + warp * 2;
   if (threadIdx.x == 0) cta_count = 0;
   __syncthreads();
@@ -1042,7 +1041,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     uint8_t* ib = wb + buf * IN_B;
     const bool full = b < n_full;
     const uint32_t nvalid = full ? G::B : static_cast<uint32_t>(a.N - b * G::B);
-    if (lane == 0) bulk_wait_read<0>();  // the previous batch's bulk store has read obuf
+    if (lane == 0) bulk_wait_read<0>();  // the previous batch's bulk stores have read obuf and sbuf
     if (full) {
       mbar_wait(&bars[buf], (it >> 1) & 1u);
     } else {  // the ragged last batch: bounded, zero-padded loads (TMA moves whole 16-byte units)
@@ -1050,12 +1049,12 @@ __global__ void __launch_bounds__(WARPS * 32)
       for (uint32_t i = lane; i < IN_B; i += 32) ib[i] = i < nbytes ? a.in[ib0 + i] : 0;
     }
     __syncwarp();
-    cnt += long_batch<M>(reinterpret_cast<const uint32_t*>(ib), obuf,
-                         a.syn != nullptr ? a.syn + b * G::B : nullptr, nvalid, lane);
+    cnt += long_batch<M>(reinterpret_cast<const uint32_t*>(ib), obuf, sbuf, nvalid, lane);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0 && full) {
       bulk_s2g(a.out + b * OUT_B, obuf, OUT_B, pol);
+      if (a.syn != nullptr) bulk_s2g(a.syn + b * SYN_B, sbuf, SYN_B, pol);
       bulk_commit();
       const uint64_t nx = b + 2 * nw;  // the input buffer is consumed: prefetch two batches ahead
       if (nx < n_full) {
@@ -1072,6 +1071,8 @@ __global__ void __launch_bounds__(WARPS * 32)
         if (i + 1 == nbytes && last_bits != 0) x &= static_cast<uint8_t>((1u << last_bits) - 1u);  // pad bits 0
         a.out[ob0 + i] = x;
       }
+      if (a.syn != nullptr)
+        for (uint32_t i = lane; i < nvalid; i += 32) a.syn[b * SYN_B + i] = sbuf[i];
     }
     __syncwarp();
   }
@@ -1095,7 +1096,7 @@ hamming_status launch_perfect_long(const LongArgs& a0, cudaStream_t st, bool acc
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   auto kfn = perfect_long_kernel<M, WARPS>;
-  const size_t smem = static_cast<size_t>(WARPS) * (2 * G::IN_BYTES + G::OUT_BYTES);
+  const size_t smem = static_cast<size_t>(WARPS) * (2 * G::IN_BYTES + G::OUT_BYTES + G::B);
   int occ = 0;
   const hamming_status rc = kernel_blocks_per_sm(reinterpret_cast<const void*>(kfn), dev, WARPS * 32, smem, true, occ);
   if (rc != HAMMING_OK) return rc;

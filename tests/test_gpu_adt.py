@@ -1,0 +1,25 @@
+"""The paper's transfer model, Eq. 1 (SPEC S:L371-409
+sdt_makespan / adt_makespan), on the library's host pipeline
+(hamming_decode_host): stage times measured per chunk
+predict the measured SDT (1 stream) and ADT (3 streams) makespans within
+15 %, and ADT beats SDT (overlap never hurts).  The full table is
+tools/adt_eq1.py -> profiles/r02_adt_eq1.md."""
+import os
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+
+@pytest.mark.parametrize("m,chunk,n_chunks", [(6, 1 << 22, 12), (4, 1 << 23, 12)])
+def test_eq1_makespans_match_measured_stages(m, chunk, n_chunks):
+    import adt_eq1
+    r = adt_eq1.model(m, chunk, n_chunks)
+    assert abs(r["sdt"] / r["sdt_pred"] - 1) < 0.15, r
+    assert abs(r["adt"] / r["adt_pred"] - 1) < 0.15, r
+    assert r["adt"] < r["sdt"] and r["speedup"] > 1.3, r
+    # the link dominates (the paper's own regime: T_PS + T_PR >= T_DKE)
+    assert r["t_ps"] + r["t_pr"] >= r["t_dke"], r

@@ -78,10 +78,9 @@ def test_every_received_word_tiled_large(oracle, m):
     many codeword slots of a lane."""
     n = 2 ** m - 1
     rng = np.random.default_rng(1000 + m)
-    blocks = max(1, ((1 << 17) + 2 ** n - 1) // 2 ** n) + 1
-    words = np.concatenate([rng.permutation(2 ** n) for _ in range(blocks)]).astype(np.int64)
-    N = (1 << 17) + 77 if m < 4 else words.size - 1234
-    words = words[:N]
+    N = (1 << 17) + 77 if m < 4 else 4 * 2 ** n + 1234
+    blocks = (N + 2 ** n - 1) // 2 ** n
+    words = np.concatenate([rng.permutation(2 ** n) for _ in range(blocks)]).astype(np.int64)[:N]
     bits = ((words[:, None] >> np.arange(n)) & 1).astype(np.uint8).reshape(-1)
     rx = np.packbits(bits, bitorder="little")
     assert_same(m, N, gpu_decode(m, rx, N), oracle.decode_mt(m, rx, N, THREADS))
