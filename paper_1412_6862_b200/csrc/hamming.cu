@@ -501,15 +501,19 @@ __device__ __forceinline__ uint32_t insert_byte1(uint32_t word, uint32_t e, int 
 }
 
 // (7,4): per-lane replicated 128-entry table of 8-byte entries {data nibble
-// replicated into all eight nibbles, syndrome}; lane l reads entry [x][l],
-// always its own bank pair (32 KB).  The replicated nibble goes to its place
-// in the output word with one LOP3 against a constant mask (no shift).
+// replicated into all eight nibbles, s | (s != 0) << 16}; lane l reads entry
+// [x][l], always its own bank pair (32 KB, conflict-free).  The replicated
+// nibble goes to its place in the output word with one LOP3 against a constant
+// mask (no shift); the syndrome bytes of four codewords become one side word by
+// three PRMTs, and the count is the high half of the plain sum of the .y words
+// (the low halves add up to at most 32 x 7, no carry into bit 16).
 struct DecodeLut3Op {
   static constexpr int NCOUNT = 1;
   __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
   static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
   static constexpr bool HAS_SIDE = true;
+  static constexpr bool LANE_COUNT = true;
   static constexpr int SHARED = 128 * 32 * 8;
   struct Args {};
 
@@ -518,27 +522,100 @@ struct DecodeLut3Op {
     for (int e = tid; e < 128 * 32; e += nth) {
       uint32_t dlo, dhi;
       const uint32_t s = decode_cw<3>(static_cast<uint32_t>(e >> 5) << 1, 0u, dlo, dhi);
-      L[e] = make_uint2(dlo * 0x11111111u, s);
+      L[e] = make_uint2(dlo * 0x11111111u, s | (static_cast<uint32_t>(s != 0) << 16));
     }
   }
 
-  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                              uint32_t (&side)[8], uint64_t, int, const Args&,
-                                              const uint8_t* sh) {
+  __device__ __forceinline__ static uint32_t lane_count(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                        uint32_t (&side)[8], uint64_t, int, const Args&,
+                                                        const uint8_t* sh) {
     uint32_t w[7];
 #pragma unroll
     for (int i = 0; i < 7; ++i) w[i] = in[i];
     __syncwarp();  // every lane has its input words: the tile may be overwritten in place
     const uint32_t lane8 = (threadIdx.x & 31u) << 3;
     uint32_t o[4] = {0, 0, 0, 0};
+    uint32_t acc = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const uint32_t off = (field_at(w, 7 * c, 8) & 0x7F00u) | lane8;  // (x * 32 + lane) * 8
-      const uint2 e = *reinterpret_cast<const uint2*>(sh + off);
-      o[c >> 3] |= e.x & (0xFu << ((4 * c) & 31));
-      side[c >> 2] |= e.y << (8 * (c & 3));
+    for (int j = 0; j < 8; ++j) {  // codewords 4j .. 4j+3
+      uint32_t y[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = 4 * j + i;
+        const uint32_t off = (field_at(w, 7 * c, 8) & 0x7F00u) | lane8;  // (x * 32 + lane) * 8
+        const uint2 e = *reinterpret_cast<const uint2*>(sh + off);
+        o[c >> 3] |= e.x & (0xFu << ((4 * c) & 31));
+        y[i] = e.y;
+      }
+      acc += y[0] + y[1] + y[2] + y[3];
+      side[j] = __byte_perm(__byte_perm(y[0], y[1], 0x0040u), __byte_perm(y[2], y[3], 0x0040u), 0x5410u);
     }
     *reinterpret_cast<uint4*>(out) = make_uint4(o[0], o[1], o[2], o[3]);
+    return acc >> 16;
+  }
+};
+
+// (7,4), two codewords per lookup: a 16384-entry table (64 KB, built per CTA)
+// indexed by the 14 stream bits of a codeword PAIR, entry = {the two corrected
+// data nibbles (byte 0), the two syndromes (bytes 1, 2), the number of nonzero
+// syndromes (byte 3)} -- every field is decode_cw<3> of one half.  Per pair:
+// one funnel shift + one LOP3 form the byte address, one LDS; the data bytes of
+// four pairs become one output word by three PRMTs, the syndrome bytes of two
+// pairs one side word by one PRMT, and the count is one add of byte 3.  The
+// per-codeword table decoder (DecodeLut3Op) spent ~5 ALU instructions per
+// codeword and bound the pipe (ncu: ALU 75 %, issue 74 %); this one ~2.
+struct DecodeLut3PairOp {
+  static constexpr int NCOUNT = 1;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&sw)[8]) { return count_nonzero_bytes_xu(sw); }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
+  static constexpr int IN_W = 7, OUT_W = 4, IN_BITS = 7;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr bool LANE_COUNT = true;  // lane_count() returns the lane's nonzero-syndrome count
+  static constexpr int SHARED = 16384 * 4 + 128 * 4;
+  struct Args {};
+
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
+    uint32_t* P = reinterpret_cast<uint32_t*>(sh);
+    uint32_t* E1 = P + 16384;  // single codewords: data | s << 8
+    for (int e = tid; e < 128; e += nth) {
+      uint32_t dlo, dhi;
+      const uint32_t s = decode_cw<3>(static_cast<uint32_t>(e) << 1, 0u, dlo, dhi);
+      E1[e] = dlo | (s << 8);
+    }
+    __syncthreads();  // cta_init is called by every thread of the CTA
+    for (int x = tid; x < 16384; x += nth) {
+      const uint32_t a = E1[x & 127], b = E1[x >> 7];
+      const uint32_t sa = a >> 8, sb = b >> 8;
+      P[x] = (a & 0xFu) | ((b & 0xFu) << 4) | (sa << 8) | (sb << 16) |
+             ((static_cast<uint32_t>(sa != 0) + static_cast<uint32_t>(sb != 0)) << 24);
+    }
+  }
+
+  __device__ __forceinline__ static uint32_t lane_count(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                        uint32_t (&side)[8], uint64_t, int, const Args&,
+                                                        const uint8_t* sh) {
+    uint32_t w[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = in[i];
+    __syncwarp();  // every lane has its input words: the tile may be overwritten in place
+    uint32_t e[16];
+#pragma unroll
+    for (int c2 = 0; c2 < 16; ++c2) {  // pair c2 = codewords 2 c2, 2 c2 + 1 = lane-stream bits 14 c2 ..
+      const uint32_t off = field_at(w, 14 * c2, 2) & 0xFFFCu;  // 4 x (14-bit index)
+      e[c2] = *reinterpret_cast<const uint32_t*>(sh + off);
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c2 = 0; c2 < 16; ++c2) cnt += e[c2] >> 24;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t t01 = __byte_perm(e[4 * i], e[4 * i + 1], 0x0040u);
+      const uint32_t t23 = __byte_perm(e[4 * i + 2], e[4 * i + 3], 0x0040u);
+      out[i] = __byte_perm(t01, t23, 0x5410u);  // data bytes of pairs 4i .. 4i+3
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) side[j] = __byte_perm(e[2 * j], e[2 * j + 1], 0x6521u);  // s of codewords 4j..4j+3
+    return cnt;
   }
 };
 
@@ -1198,6 +1275,29 @@ struct SwizzledOut<Op, decltype(void(Op::SWZ_OUT))> {
   static constexpr bool value = Op::SWZ_OUT;
 };
 
+// Ops that count inside the lane function (LANE_COUNT) return the count from
+// lane_count(); the others are counted from their side words by count0().
+template <class Op, class = void>
+struct LaneCount {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct LaneCount<Op, decltype(void(Op::LANE_COUNT))> {
+  static constexpr bool value = Op::LANE_COUNT;
+};
+
+template <class Op>
+__device__ __forceinline__ uint32_t run_lane(const uint32_t* in, uint32_t* out, uint32_t (&side)[8], uint64_t g,
+                                             int valid, const typename Op::Args& args, const uint8_t* sh) {
+  if constexpr (LaneCount<Op>::value) {
+    return Op::lane_count(in, out, side, g, valid, args, sh);
+  } else {
+    Op::lane(in, out, side, g, valid, args, sh);
+    if constexpr (Op::HAS_SIDE) return Op::count0(side);
+    return 0;
+  }
+}
+
 template <class Op>
 struct TileBytes {
   static constexpr int IN = Op::IN_W * 128;   // 32 lanes x IN_W words x 4 B
@@ -1271,8 +1371,8 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
   }
   const int valid = max(0, min(32, static_cast<int>(rem) - lane * 32));
   uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  Op::lane(reinterpret_cast<const uint32_t*>(ibuf) + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W),
-           obuf + lane * Op::OUT_W, sidew, tile * kTileCw + lane * 32, valid, args, sh);
+  const uint32_t lc = run_lane<Op>(reinterpret_cast<const uint32_t*>(ibuf) + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W),
+                                   obuf + lane * Op::OUT_W, sidew, tile * kTileCw + lane * 32, valid, args, sh);
   __syncwarp();
   const uint64_t ob0 = tile * OUT;
   const uint64_t nbo = out_total - ob0;
@@ -1291,7 +1391,7 @@ __device__ __noinline__ uint32_t run_tail_tile(const uint8_t* __restrict__ in, u
       uint8_t* sp = side + tile * kTileCw + lane * 32;
       for (int c = 0; c < valid; ++c) sp[c] = static_cast<uint8_t>(sidew[c >> 2] >> (8 * (c & 3)));
     }
-    cnt = Op::count0(sidew);  // codewords past `valid` decode zeros: s = 0, no flags
+    cnt = lc;  // codewords past `valid` decode zeros: s = 0, no flags
     if constexpr (Op::NCOUNT > 1) cnt2 += Op::count1(sidew);
   }
   return cnt;
@@ -1412,10 +1512,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   };
 
   if (threadIdx.x < 2) block_cnt[threadIdx.x] = 0;
-  if constexpr (Op::SHARED > 0) {
-    Op::cta_init(sh, threadIdx.x, blockDim.x);
-    __syncthreads();
-  }
   uint32_t stage_tile = kNoTile;  // lane s: the tile in stage s
   if constexpr (IN > 0) {
     if (lane == 0) {
@@ -1430,6 +1526,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if (lane == 0 && t != kNoTile) load_tile<Op>(wbase + s * IN, in, t, &bars[s], args, pol);
     }
     __syncwarp();
+  }
+
+  // the CTA's tables are built while the first tiles are in flight (the
+  // prologue's TMA loads land in the warp stages, disjoint from the tables)
+  if constexpr (Op::SHARED > 0) {
+    Op::cta_init(sh, threadIdx.x, blockDim.x);
+    __syncthreads();
   }
 
   uint32_t cnt = 0, cnt2 = 0;
@@ -1458,8 +1561,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
     uint32_t sidew[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint32_t* ibuf = reinterpret_cast<const uint32_t*>(wbase + st * IN);
-    Op::lane(ibuf + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W), obuf + lane * Op::OUT_W, sidew,
-             t * kTileCw + lane * 32, 32, args, sh);
+    const uint32_t lc = run_lane<Op>(ibuf + (TileBytes<Op>::SWZ ? 0 : lane * Op::IN_W), obuf + lane * Op::OUT_W,
+                                     sidew, t * kTileCw + lane * 32, 32, args, sh);
     fence_proxy_async_smem();  // make this lane's st.shared visible to the bulk copy
     __syncwarp();
     if (lane == 0) {
@@ -1491,7 +1594,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         st_global_cs_v4(sp, sidew[0], sidew[1], sidew[2], sidew[3]);
         st_global_cs_v4(sp + 16, sidew[4], sidew[5], sidew[6], sidew[7]);
       }
-      cnt += Op::count0(sidew);
+      cnt += lc;
       if constexpr (Op::NCOUNT > 1) cnt2 += Op::count1(sidew);
     }
   }
@@ -1817,6 +1920,9 @@ bool bits_overflow(int m, uint64_t N) {
 #ifndef HAM_S3
 #define HAM_S3 12
 #endif
+#ifndef HAM_M3_OP
+#define HAM_M3_OP DecodeLut3Op
+#endif
 #ifndef HAM_IP3
 #define HAM_IP3 true
 #endif
@@ -1930,7 +2036,7 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
       return Launcher<DecodeOp<2>, HAM_W2, HAM_S2, HAM_IP2>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                  accumulate);
     case 3:
-      return Launcher<DecodeLut3Op, HAM_W3, HAM_S3, HAM_IP3>::run(in, out, syn, N, ib, ob, counter, {}, st,
+      return Launcher<HAM_M3_OP, HAM_W3, HAM_S3, HAM_IP3>::run(in, out, syn, N, ib, ob, counter, {}, st,
                                                                   accumulate, HAM_DYN3);
     case 4: {
       int dev = 0;
@@ -1978,9 +2084,58 @@ HostSlotLayout host_slot_layout(int m, uint64_t chunk, int with_syn) {
 }  // namespace
 
 // =================================================================== C ABI
+#ifdef HAM_PROBE
+// ------------------------------------------------ power/bandwidth probes
+// Tools-only build (-DHAM_PROBE, tools/power_probe.py): the (63,57) tile
+// pipeline with the decode taken out, to split the decode's power between
+// the TMA round trip through shared memory and the arithmetic.
+//   kind 0 (ProbeTmaOp): the lane does nothing -- TMA in, the first 57 x 128
+//     bytes of the tile TMA out, zero syndrome bytes stored: the same HBM
+//     bytes as the decode, no shared-memory loads or stores by the SM.
+//   kind 1 (ProbeLdsOp): the lane also loads its 63 words from shared memory
+//     and stores 57 of them back (the decode's LDS/STS traffic, no math).
+struct ProbeTmaOp {
+  static constexpr int NCOUNT = 1;
+  __device__ __forceinline__ static uint32_t count0(const uint32_t (&)[8]) { return 0; }
+  __device__ __forceinline__ static uint32_t count1(const uint32_t (&)[8]) { return 0; }
+  static constexpr int IN_W = 63, OUT_W = 57, IN_BITS = 63;
+  static constexpr bool HAS_SIDE = true;
+  static constexpr int SHARED = 0;
+  struct Args {};
+  __device__ __forceinline__ static void cta_init(uint8_t*, int, int) {}
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__, uint32_t* __restrict__, uint32_t (&)[8],
+                                              uint64_t, int, const Args&, const uint8_t*) {}
+};
+struct ProbeLdsOp : ProbeTmaOp {
+  __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                              uint32_t (&side)[8], uint64_t, int, const Args&, const uint8_t*) {
+    uint32_t w[63];
+#pragma unroll
+    for (int i = 0; i < 63; ++i) w[i] = in[i];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 57; ++i) out[i] = w[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) side[i] = w[57 + i % 6] & 0x01010101u;
+  }
+};
+#endif
+
 extern "C" {
 
 int hamming_abi_version(void) { return HAMMING_ABI_VERSION; }
+
+#ifdef HAM_PROBE
+hamming_status hamming_probe_tiles(int kind, const void* rx_dev, uint64_t N, void* data_dev, uint8_t* syn_dev,
+                                   unsigned long long* counter, void* stream) {
+  const uint64_t ib = (63 * N + 7) / 8, ob = (57 * N + 7) / 8;
+  const auto* in = static_cast<const uint8_t*>(rx_dev);
+  auto* out = static_cast<uint8_t*>(data_dev);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (kind == 0) return Launcher<ProbeTmaOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn_dev, N, ib, ob, counter, {}, st);
+  return Launcher<ProbeLdsOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn_dev, N, ib, ob, counter, {}, st);
+}
+#endif
 #ifdef HAM_TIMING
 int hamming_debug_timing(unsigned long long* host_out, int n) {
   return cudaMemcpyFromSymbol(host_out, g_timing, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;

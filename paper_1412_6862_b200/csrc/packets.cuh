@@ -395,6 +395,14 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T, bool al
   return HAMMING_OK;
 }
 
+// word descriptors in shared memory: Wp of them, padded with zero descriptors
+// (d.w = 0: skipped) to whole steps of pass R's unrolled np = 1 loop, so that
+// loop needs no bounds test
+constexpr uint32_t kPktRU = 4;
+__host__ __device__ constexpr uint32_t pkt_wdesc_entries(uint32_t Wp) {
+  return (Wp + 32 * kPktRU - 1) / (32 * kPktRU) * (32 * kPktRU);
+}
+
 struct BatchGeom {
   uint32_t warps;      // warps per CTA (<= kPktWarps)
   uint32_t G;          // packets per batch
@@ -479,7 +487,7 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
   b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
                  static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
-  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
+  b.tab_bytes = (16 * pkt_wdesc_entries(T.Wp) + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
   // a padded stride (any multiple of 16 >= the coded bytes is legal) can make the
   // shape's warps overflow shared memory: fewer warps per CTA then (the kernel
   // takes its warp count from blockDim)
@@ -578,10 +586,15 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
   // pieces {src | len | pos, word}, per-segment geometry
   uint4* wdesc = reinterpret_cast<uint4*>(smem);
-  uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * Wp);
+  const uint32_t WpPad = pkt_wdesc_entries(Wp);
+  uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * WpPad);
   uint2* spec = pieces + T.n_pieces;  // head words {word, first piece | end piece << 16}
   uint32_t* sg = reinterpret_cast<uint32_t*>(spec + T.n_special);  // [off | n | k | moff] x kPktMaxSeg
-  for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
+  for (uint32_t i = threadIdx.x; i < WpPad; i += blockDim.x) {
+    if (i >= Wp) {
+      wdesc[i] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
     const bool head = nb > 32;  // head words: pass R skips them (pass H, or with HX pass X, writes them)
     // .w: the shift of slice 1 (1..32, the skipped parity bit), 0 for a head word (pass R skips it)
@@ -715,24 +728,44 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       }
     }
     __syncwarp();
-    {  // pass R: every word as one or two slices (lane: word W of every packet of the batch)
+    {  // pass R: every word as one or two slices (lane: word W of every packet of the batch).
+       // Loads are issued kRU words (or packets) at a time before any store, so a
+       // warp has kRU independent shared-memory round trips in flight instead of one
+       // (the stores go to the message buffer, which no load of this pass reads).
+      constexpr uint32_t kRU = kPktRU;
       const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
-      if (np == 1) {  // one packet per batch (long packets): no inner loop
-        for (uint32_t W = lane; W < Wp; W += 32) {
-          const uint4 d = wdesc[W];
-          const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
-          if (d.w) mbuf[W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
+      // slice 1 is the stream one bit further on (the parity position skipped)
+      auto rr = [](uint32_t a0, uint32_t a1, const uint4& d) {
+        return (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
+      };
+      if (np == 1) {  // one packet per batch (long packets): kRU words per lane per step
+        for (uint32_t W0 = lane; W0 < Wp; W0 += 32 * kRU) {
+          uint4 d[kRU];
+          uint32_t x0[kRU], x1[kRU];
+#pragma unroll
+          for (uint32_t u = 0; u < kRU; ++u) d[u] = wdesc[W0 + 32 * u];  // zero past Wp (padded)
+#pragma unroll
+          for (uint32_t u = 0; u < kRU; ++u) x0[u] = w[4 + d[u].x], x1[u] = w[5 + d[u].x];
+#pragma unroll
+          for (uint32_t u = 0; u < kRU; ++u)
+            if (d[u].w) mbuf[W0 + 32 * u] = rr(x0[u], x1[u], d[u]);  // d.w = 0: head word or past Wp
         }
       } else {
         for (uint32_t W = lane; W < T.Wfull; W += 32) {
           const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, shift + 1 (0: head word)}
+          if (d.w == 0) continue;    // a head word: pass X (or H) writes it
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
           uint32_t* mp = mbuf + W;
-          for (uint32_t p = 0; p < np; ++p, wp += wstride, mp += Wp) {
-            const uint32_t a0 = wp[0], a1 = wp[1];
-            // slice 1 is the stream one bit further on (the parity position skipped)
-            if (d.w) *mp = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
+          uint32_t p = 0;
+          for (; p + kRU <= np; p += kRU, wp += kRU * wstride, mp += kRU * Wp) {
+            uint32_t x0[kRU], x1[kRU];
+#pragma unroll
+            for (uint32_t u = 0; u < kRU; ++u) x0[u] = wp[u * wstride], x1[u] = wp[u * wstride + 1];
+#pragma unroll
+            for (uint32_t u = 0; u < kRU; ++u) mp[u * Wp] = rr(x0[u], x1[u], d);
           }
+#pragma unroll 1
+          for (; p < np; ++p, wp += wstride, mp += Wp) *mp = rr(wp[0], wp[1], d);
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
         #pragma unroll 1
@@ -743,7 +776,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];
           const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          if (d.w) mbuf[p * Wp + W] = (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
+          if (d.w) mbuf[p * Wp + W] = rr(a0, a1, d);
         }
       }
     }

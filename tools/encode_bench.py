@@ -2,6 +2,7 @@
 encoder: min of 8 launches on 2 GiB of coded output per m.
     python tools/encode_bench.py [--m 3 4 5 6] [--gib 2]"""
 import argparse
+import json
 import os
 import sys
 
@@ -14,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, nargs="+", default=[3, 4, 5, 6])
 ap.add_argument("--gib", type=float, default=2.0)
 a = ap.parse_args()
-peak = 6548.2
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 for secded in (False, True):
     for m in a.m:
         n, k = ham.code_nk(m)

@@ -7,7 +7,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-OUT = os.path.join(ROOT, "build", "tune")
+OUT = os.path.join(ROOT, "tune_libs")  # ships to the GPU box (build/ is gpurun-ignored)
 
 VARIANTS = {
     # m: list of (W, S, in_place)
@@ -32,7 +32,10 @@ SECDED_VARIANTS = {
     5: [(12, 3), (8, 4), (16, 2), (8, 3)],
     6: [(8, 3), (12, 2), (8, 2)],
 }
-PKT_VARIANTS = [(b, st, mb, w) for b, st, mb, w in ((6144, 2, 1, 16), (13312, 2, 1, 8), (9216, 2, 1, 8), (7168, 2, 1, 8), (9216, 2, 1, 12), (6656, 2, 1, 12))]
+M3_VARIANTS = [("DecodeLut3Op", 16, 12), ("DecodeLut3Op", 32, 6), ("DecodeLut3Op", 24, 8),
+               ("DecodeLut3PairOp", 16, 10), ("DecodeLut3PairOp", 16, 3), ("DecodeLut3PairOp", 32, 5),
+               ("DecodeLut3PairOp", 24, 6)]
+PKT_VARIANTS = [(6144, 2, 1, 16), (9216, 2, 1, 12), (12416, 2, 1, 8), (12416, 2, 1, 16), (18560, 2, 1, 8), (18560, 2, 1, 12), (24704, 2, 1, 8)]
 
 
 def name(m, v):
@@ -45,6 +48,8 @@ def build():
     from paper_1412_6862_b200 import build as b
     os.makedirs(OUT, exist_ok=True)
     for f in os.listdir(OUT):
+        if not (len(sys.argv) > 2 and sys.argv[2] == "m3" and f.startswith("m3_")):
+            continue
         os.remove(os.path.join(OUT, f))
     jobs = []
     for m, vs in VARIANTS.items():
@@ -59,9 +64,15 @@ def build():
         jobs = [(os.path.join(OUT, f"sec_m{m}_w{w}_s{st}.so"), [f"HAM_SEC_W{m}={w}", f"HAM_SEC_S{m}={st}"])
                 for m, vs in SECDED_VARIANTS.items() for w, st in vs]
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
+        for f in os.listdir(OUT):
+            if f.startswith("pkt_"):
+                os.remove(os.path.join(OUT, f))
         jobs = [(os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"),
                  [f"HAM_PKT_BUDGET={b}", f"HAM_PKT_STAGES={st}", f"HAM_PKT_MSGBUF={mb}", f"HAM_PKT_WARPS={w}"])
                 for b, st, mb, w in PKT_VARIANTS]
+    if len(sys.argv) > 2 and sys.argv[2] == "m3":
+        jobs = [(os.path.join(OUT, f"m3_{op}_w{w}_s{st}.so"), [f"HAM_M3_OP={op}", f"HAM_W3={w}", f"HAM_S3={st}"])
+                for op, w, st in M3_VARIANTS]
     with ThreadPoolExecutor(os.cpu_count() or 4) as ex:
         for path in ex.map(lambda j: b.build(force=True, out=j[0], defines=j[1]), jobs):
             print("built", path, flush=True)
@@ -82,12 +93,19 @@ def run():
                 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--secded", "--m",
                                 str(m), "--tag", f"w{w}_s{st}"], env=env)
         return
+    if len(sys.argv) > 2 and sys.argv[2] == "m3":
+        for op, w, st in M3_VARIANTS:
+            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"m3_{op}_w{w}_s{st}.so"))
+            for gib in ("2", "0.25"):
+                subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--m", "3", "--gib", gib,
+                                "--tag", f"{op}_w{w}_s{st}"], env=env)
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "packets":
         for b, st, mb, w in PKT_VARIANTS:
             env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"))
             print("budget", b, "stages", st, "msgbufs", mb, "warps", w, flush=True)
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "800", "1200", "1600",
-                            "2000", "--t", "2", "3", "6"], env=env)
+                            "2000", "--t", "2", "5"], env=env)
         return
     for m, vs in VARIANTS.items():
         for v in vs:
