@@ -95,7 +95,44 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef HAM_WAIT_MODE
+#define HAM_WAIT_MODE 0
+#endif
+#ifndef HAM_WAIT_NS
+#define HAM_WAIT_NS 100000
+#endif
+// Wait for an mbarrier phase.  Mode 0: the try_wait loop (the hardware may
+// suspend the thread inside try_wait for a system-dependent time); mode 1:
+// try_wait with an explicit suspend-time hint (HAM_WAIT_NS); mode 2: a failed
+// try_wait backs off with __nanosleep(HAM_WAIT_NS) -- modes 1, 2 are power
+// experiments (tools/power_probe.py).
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if HAM_WAIT_MODE == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "HAM_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra HAM_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase), "r"(HAM_WAIT_NS)
+      : "memory");
+#elif HAM_WAIT_MODE == 2
+  while (!mbar_try(bar, phase)) __nanosleep(HAM_WAIT_NS);
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -105,6 +142,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "}\n" ::"r"(smem_addr(bar)),
       "r"(phase)
       : "memory");
+#endif
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
@@ -1730,6 +1768,9 @@ int g_slots_used[kMaxDev];
 
 LaunchSlot* launch_slot(int dev, cudaStream_t st) {
   if (dev < 0 || dev >= kMaxDev) return nullptr;
+  // the per-thread default stream has one handle value for every host thread's
+  // own stream: launches from two threads could run at once on one slot
+  if (st == cudaStreamPerThread) return nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
@@ -2119,6 +2160,18 @@ struct ProbeLdsOp : ProbeTmaOp {
     for (int i = 0; i < 8; ++i) side[i] = w[57 + i % 6] & 0x01010101u;
   }
 };
+// kind 3 (ProbeCopyTileOp): whole (63,57)-sized tiles TMA in and the same
+//   tile TMA out, no side stores: a TMA copy through shared memory.
+// kind 4: a plain grid-stride LDG.128 / STG.128 copy kernel (no shared memory).
+struct ProbeCopyTileOp : ProbeTmaOp {
+  static constexpr int OUT_W = 63;
+  static constexpr bool HAS_SIDE = false;
+};
+__global__ void probe_copy_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, uint64_t n16) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
 #endif
 
 extern "C" {
@@ -2133,7 +2186,13 @@ hamming_status hamming_probe_tiles(int kind, const void* rx_dev, uint64_t N, voi
   auto* out = static_cast<uint8_t*>(data_dev);
   auto st = static_cast<cudaStream_t>(stream);
   if (kind == 0) return Launcher<ProbeTmaOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn_dev, N, ib, ob, counter, {}, st);
-  return Launcher<ProbeLdsOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn_dev, N, ib, ob, counter, {}, st);
+  if (kind == 1) return Launcher<ProbeLdsOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, syn_dev, N, ib, ob, counter, {}, st);
+  if (kind == 2) return Launcher<ProbeTmaOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, nullptr, N, ib, ob, counter, {}, st);
+  // kinds 3, 4 move ib + ob + N bytes too: ib read and (ob + N) ~ ib written (the same HBM volume)
+  if (kind == 3) return Launcher<ProbeCopyTileOp, HAM_W6, HAM_S6, HAM_IP6>::run(in, out, nullptr, N, ib, ib, nullptr, {}, st);
+  const uint64_t n16 = ib / 16;
+  probe_copy_kernel<<<148 * 8, 512, 0, st>>>(reinterpret_cast<const uint4*>(in), reinterpret_cast<uint4*>(out), n16);
+  return cudaGetLastError() == cudaSuccess ? HAMMING_OK : HAMMING_E_CUDA;
 }
 #endif
 #ifdef HAM_TIMING

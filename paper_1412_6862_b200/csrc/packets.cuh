@@ -395,13 +395,8 @@ hamming_status build_packet_tables(const PacketGeom& g, PacketTables& T, bool al
   return HAMMING_OK;
 }
 
-// word descriptors in shared memory: Wp of them, padded with zero descriptors
-// (d.w = 0: skipped) to whole steps of pass R's unrolled np = 1 loop, so that
-// loop needs no bounds test
+// pass R: words (np = 1) or packets (np > 1) per unrolled step
 constexpr uint32_t kPktRU = 4;
-__host__ __device__ constexpr uint32_t pkt_wdesc_entries(uint32_t Wp) {
-  return (Wp + 32 * kPktRU - 1) / (32 * kPktRU) * (32 * kPktRU);
-}
 
 struct BatchGeom {
   uint32_t warps;      // warps per CTA (<= kPktWarps)
@@ -487,7 +482,7 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
   // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
   b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
                  static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
-  b.tab_bytes = (16 * pkt_wdesc_entries(T.Wp) + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
+  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
   // a padded stride (any multiple of 16 >= the coded bytes is legal) can make the
   // shape's warps overflow shared memory: fewer warps per CTA then (the kernel
   // takes its warp count from blockDim)
@@ -586,15 +581,10 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   // CTA tables: word descriptors {word, shift, mask of slice 0, keep}, head-word
   // pieces {src | len | pos, word}, per-segment geometry
   uint4* wdesc = reinterpret_cast<uint4*>(smem);
-  const uint32_t WpPad = pkt_wdesc_entries(Wp);
-  uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * WpPad);
+  uint2* pieces = reinterpret_cast<uint2*>(smem + 16 * Wp);
   uint2* spec = pieces + T.n_pieces;  // head words {word, first piece | end piece << 16}
   uint32_t* sg = reinterpret_cast<uint32_t*>(spec + T.n_special);  // [off | n | k | moff] x kPktMaxSeg
-  for (uint32_t i = threadIdx.x; i < WpPad; i += blockDim.x) {
-    if (i >= Wp) {
-      wdesc[i] = make_uint4(0, 0, 0, 0);
-      continue;
-    }
+  for (uint32_t i = threadIdx.x; i < Wp; i += blockDim.x) {
     const uint32_t s0 = T.word0[i] & 0xFFFFu, nb = T.word0[i] >> 16;
     const bool head = nb > 32;  // head words: pass R skips them (pass H, or with HX pass X, writes them)
     // .w: the shift of slice 1 (1..32, the skipped parity bit), 0 for a head word (pass R skips it)
@@ -738,17 +728,24 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       auto rr = [](uint32_t a0, uint32_t a1, const uint4& d) {
         return (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
       };
-      if (np == 1) {  // one packet per batch (long packets): kRU words per lane per step
-        for (uint32_t W0 = lane; W0 < Wp; W0 += 32 * kRU) {
+      if (np == 1) {  // one packet per batch (long packets): kRU words per lane per step, then single words
+        const uint32_t Wstep = Wp / (32 * kRU) * (32 * kRU);
+        for (uint32_t W0 = lane; W0 < Wstep; W0 += 32 * kRU) {
           uint4 d[kRU];
           uint32_t x0[kRU], x1[kRU];
 #pragma unroll
-          for (uint32_t u = 0; u < kRU; ++u) d[u] = wdesc[W0 + 32 * u];  // zero past Wp (padded)
+          for (uint32_t u = 0; u < kRU; ++u) d[u] = wdesc[W0 + 32 * u];
 #pragma unroll
           for (uint32_t u = 0; u < kRU; ++u) x0[u] = w[4 + d[u].x], x1[u] = w[5 + d[u].x];
 #pragma unroll
           for (uint32_t u = 0; u < kRU; ++u)
-            if (d[u].w) mbuf[W0 + 32 * u] = rr(x0[u], x1[u], d[u]);  // d.w = 0: head word or past Wp
+            if (d[u].w) mbuf[W0 + 32 * u] = rr(x0[u], x1[u], d[u]);  // d.w = 0: a head word
+        }
+#pragma unroll 1
+        for (uint32_t W = Wstep + lane; W < Wp; W += 32) {
+          const uint4 d = wdesc[W];
+          const uint32_t a0 = w[4 + d.x], a1 = w[5 + d.x];
+          if (d.w) mbuf[W] = rr(a0, a1, d);
         }
       } else {
         for (uint32_t W = lane; W < T.Wfull; W += 32) {

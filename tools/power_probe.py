@@ -72,7 +72,8 @@ def run(name, fn, nbytes, seconds=3.0):
 G = 8 << 30
 a = torch.empty(G // 2, dtype=torch.uint8, device="cuda")
 b = torch.empty(G // 2, dtype=torch.uint8, device="cuda")
-run("copy 4 GiB -> 4 GiB", lambda: b.copy_(a), G)
+if "--no-copy" not in sys.argv:
+    run("copy 4 GiB -> 4 GiB", lambda: b.copy_(a), G)
 del a, b
 if PROBE:
     L = _lib.lib()
@@ -80,16 +81,19 @@ if PROBE:
                                       ctypes.c_void_p, ctypes.c_void_p]
     N = (4 << 30) * 8 // 63 // 1024 * 1024
     rx = torch.empty(ham.coded_bytes(6, N), dtype=torch.uint8, device="cuda").random_(0, 256)
-    out = torch.empty(ham.data_bytes(6, N), dtype=torch.uint8, device="cuda")
+    out = torch.empty(ham.coded_bytes(6, N), dtype=torch.uint8, device="cuda")  # kinds 3, 4 write ib bytes
     syn = torch.empty(N, dtype=torch.uint8, device="cuda")
     cnt = torch.empty(1, dtype=torch.int64, device="cuda")
     alg = ham.coded_bytes(6, N) + ham.data_bytes(6, N) + N
-    for kind, nm in ((0, "probe TMA only (63,57) tiles"), (1, "probe TMA + LDS/STS")):
+    kinds = ((0, "probe TMA only (63,57) tiles"), (1, "probe TMA + LDS/STS"), (2, "probe TMA only, no syndromes"),
+             (3, "probe TMA copy (63-word tiles)"), (4, "probe LDG/STG copy"))
+    for kind, nm in kinds:
         def fn(kind=kind):
             rc = L.hamming_probe_tiles(kind, rx.data_ptr(), N, out.data_ptr(), syn.data_ptr(), cnt.data_ptr(),
                                        torch.cuda.current_stream().cuda_stream)
             assert rc == 0, rc
-        run(nm, fn, alg)
+        # kind 2 writes no syndrome bytes; kinds 3, 4 read and write the coded bytes
+        run(nm, fn, alg - N if kind == 2 else (2 * ham.coded_bytes(6, N) if kind >= 3 else alg))
     del rx, out, syn
     torch.cuda.empty_cache()
 for m in ((6,) if ONLY6 else (6, 5, 4, 3)):

@@ -35,6 +35,8 @@ SECDED_VARIANTS = {
 M3_VARIANTS = [("DecodeLut3Op", 16, 12), ("DecodeLut3Op", 32, 6), ("DecodeLut3Op", 24, 8),
                ("DecodeLut3PairOp", 16, 10), ("DecodeLut3PairOp", 16, 3), ("DecodeLut3PairOp", 32, 5),
                ("DecodeLut3PairOp", 24, 6)]
+# (63,57) decode and the probe ops (-DHAM_PROBE) at several shapes, for the sustained power probe
+POWER6_VARIANTS = [(8, 3, 0, 0), (8, 3, 1, 100000), (8, 3, 1, 2000), (8, 3, 2, 32), (8, 3, 2, 256), (8, 3, 2, 1000)]
 PKT_VARIANTS = [(6144, 2, 1, 16), (9216, 2, 1, 12), (12416, 2, 1, 8), (12416, 2, 1, 16), (18560, 2, 1, 8), (18560, 2, 1, 12), (24704, 2, 1, 8)]
 
 
@@ -70,6 +72,10 @@ def build():
         jobs = [(os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"),
                  [f"HAM_PKT_BUDGET={b}", f"HAM_PKT_STAGES={st}", f"HAM_PKT_MSGBUF={mb}", f"HAM_PKT_WARPS={w}"])
                 for b, st, mb, w in PKT_VARIANTS]
+    if len(sys.argv) > 2 and sys.argv[2] == "power6":
+        jobs = [(os.path.join(OUT, f"pw6_w{w}_s{st}_m{md}_{ns}.so"),
+                 ["HAM_PROBE", f"HAM_W6={w}", f"HAM_S6={st}", f"HAM_WAIT_MODE={md}", f"HAM_WAIT_NS={ns}"])
+                for w, st, md, ns in POWER6_VARIANTS]
     if len(sys.argv) > 2 and sys.argv[2] == "m3":
         jobs = [(os.path.join(OUT, f"m3_{op}_w{w}_s{st}.so"), [f"HAM_M3_OP={op}", f"HAM_W3={w}", f"HAM_S3={st}"])
                 for op, w, st in M3_VARIANTS]
@@ -92,6 +98,13 @@ def run():
                 env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"sec_m{m}_w{w}_s{st}.so"))
                 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--secded", "--m",
                                 str(m), "--tag", f"w{w}_s{st}"], env=env)
+        return
+    if len(sys.argv) > 2 and sys.argv[2] == "power6":
+        for w, st, md, ns in POWER6_VARIANTS:
+            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pw6_w{w}_s{st}_m{md}_{ns}.so"))
+            print(f"== shape W={w} S={st} wait mode {md} ({ns} ns)", flush=True)
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "power_probe.py"), "--probe", "--only6",
+                            "--no-copy"], env=env)
         return
     if len(sys.argv) > 2 and sys.argv[2] == "m3":
         for op, w, st in M3_VARIANTS:
