@@ -607,27 +607,28 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   uint64_t* bars = bars_all + warp * kPktStages;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t n_batches = (a.n_packets + bg.G - 1) / bg.G;
-  const uint64_t gw = static_cast<uint64_t>(warp) * gridDim.x + blockIdx.x;  // CTA-minor (see tiles_kernel)
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  // one launch covers fewer than 2^31 packets (the host splits larger calls), so the batch
+  // arithmetic is 32-bit; only the global addresses are 64-bit
+  const uint32_t nP = static_cast<uint32_t>(a.n_packets);
+  const uint32_t n_batches = (nP + bg.G - 1) / bg.G;
+  const uint32_t gw = static_cast<uint32_t>(warp) * gridDim.x + blockIdx.x;  // CTA-minor (see tiles_kernel)
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   const uint64_t pol = policy_evict_first();
   const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
   const uint32_t groups = 32 / L;
   const uint32_t stride_bits = static_cast<uint32_t>(a.in_stride * 8);
+  const uint32_t in_stride = static_cast<uint32_t>(a.in_stride);
   uint32_t n_corr = 0, n_fail = 0;
-  auto batch_bytes = [&](uint64_t b) -> uint32_t {
-    const uint64_t p0 = b * bg.G;
-    const uint64_t left = a.n_packets - p0;
-    return static_cast<uint32_t>((left < bg.G ? left : bg.G) * a.in_stride);
-  };
+  auto batch_bytes = [&](uint32_t b) -> uint32_t { return min(nP - b * bg.G, bg.G) * in_stride; };
+  auto batch_src = [&](uint32_t b) { return a.in + static_cast<uint64_t>(b) * bg.G * in_stride; };
   if (lane == 0) {
     for (uint32_t s = 0; s < kPktStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
     for (uint32_t s = 0; s < kPktStages; ++s) {
-      const uint64_t b = gw + s * nw;
+      const uint32_t b = gw + s * nw;
       if (b < n_batches) {
         mbar_arrive_expect_tx(&bars[s], batch_bytes(b));
-        bulk_g2s(wb + s * bg.in_cap + 16, a.in + b * bg.G * a.in_stride, batch_bytes(b), &bars[s], pol);
+        bulk_g2s(wb + s * bg.in_cap + 16, batch_src(b), batch_bytes(b), &bars[s], pol);
       }
     }
   }
@@ -637,13 +638,13 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   const bool bulk_out = a.out_stride == g.msg_bytes && (g.msg_bytes & 15u) == 0 &&
                         (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0;
   uint32_t it = 0;
-  for (uint64_t b = gw; b < n_batches; b += nw, ++it) {
+  for (uint32_t b = gw; b < n_batches; b += nw, ++it) {
     const uint32_t buf = it % kPktStages;
     const uint32_t* w = reinterpret_cast<const uint32_t*>(wb + buf * bg.in_cap);
-    const uint64_t p0 = b * bg.G;
-    const uint64_t left = a.n_packets - p0;
-    const uint32_t np = static_cast<uint32_t>(left < bg.G ? left : bg.G);
+    const uint32_t p0 = b * bg.G;
+    const uint32_t np = min(nP - p0, bg.G);
     uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + (it % kPktMsgBufs) * bg.msg_cap);
+    uint16_t* syn_b = a.syn != nullptr ? a.syn + static_cast<uint64_t>(p0) * g.t : nullptr;
     if (lane == 0) bulk_wait_read<kPktMsgBufs - 1>();  // the bulk store that last used this mbuf has read it
     // G <= 64: two predicated stores (a lane-strided loop here compiles to ~40 instructions of unroll set-up)
     if (static_cast<uint32_t>(lane) < np) pst[lane] = 0;
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         if (lead) {
           const bool corr = s != 0 && s <= n;
           const bool fail = s > n;
-          if (a.syn != nullptr) a.syn[(p0 + pk) * g.t + seg] = static_cast<uint16_t>(s);
+          if (syn_b != nullptr) syn_b[pk * g.t + seg] = static_cast<uint16_t>(s);
           if (corr || fail) atomicMax(&pst[pk], fail ? 2u : 1u);
           n_corr += corr;
           n_fail += fail;
@@ -798,15 +799,15 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     }
     __syncwarp();
     if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
-      const uint64_t nx = b + kPktStages * nw;
+      const uint32_t nx = b + kPktStages * nw;
       if (nx < n_batches) {
         mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
-        bulk_g2s(wb + buf * bg.in_cap + 16, a.in + nx * bg.G * a.in_stride, batch_bytes(nx), &bars[buf], pol);
+        bulk_g2s(wb + buf * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[buf], pol);
       }
     }
     // write the batch's messages (packet pk at word pk * Wp of mbuf) and statuses
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
-    const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + p0 * a.out_stride);
+    const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + static_cast<uint64_t>(p0) * a.out_stride);
     if (bulk_out) {
       fence_proxy_async_smem();  // this lane's st.shared / atomics visible to the bulk copy
       __syncwarp();
@@ -885,15 +886,25 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   int occ = 0;
   rc = kernel_blocks_per_sm(reinterpret_cast<const void*>(kfn), dev, bg.warps * 32, smem, true, occ);
   if (rc != HAMMING_OK) return rc;
-  const uint64_t batches = (a.n_packets + bg.G - 1) / bg.G;
-  const uint64_t want = (batches + bg.warps - 1) / bg.warps;
-  const int grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
-  if (grid > 0) {
-    kfn<<<grid, bg.warps * 32, smem, st>>>(g, bg, a, T);
+  // the kernel's batch arithmetic is 32-bit: one launch per 2^31 packets (counts accumulate)
+  constexpr uint64_t kMaxPackets = 1ull << 31;
+  int launches = 0, grid = 0;
+  for (uint64_t first = 0; first < a.n_packets; first += kMaxPackets) {
+    PacketArgs c = a;
+    c.n_packets = std::min(kMaxPackets, a.n_packets - first);
+    c.in = a.in + first * a.in_stride;
+    c.out = a.out + first * a.out_stride;
+    if (a.syn != nullptr) c.syn = a.syn + first * g.t;
+    if (a.status != nullptr) c.status = a.status + first;
+    const uint64_t batches = (c.n_packets + bg.G - 1) / bg.G;
+    const uint64_t want = (batches + bg.warps - 1) / bg.warps;
+    grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+    kfn<<<grid, bg.warps * 32, smem, st>>>(g, bg, c, T);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "packets decode launch");
+    ++launches;
   }
-  g_launches = grid > 0 ? 1 : 0;
+  g_launches = launches;
   g_grid = grid;
   return HAMMING_OK;
 }
