@@ -193,6 +193,17 @@ hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t *seg_k_
  *   8-byte aligned (HAMMING_E_MISALIGNED); no two of rx, msg, syndromes,
  *   status, counts may overlap (HAMMING_E_OVERLAP).  All checks return
  *   before any launch. */
+/* hamming_packet_launch_shape -- host only, no CUDA call: the launch shape
+ * hamming_decode_packets would use for n_packets packets at rx_stride on a
+ * GPU with sm_count SMs (the issue model): warps per CTA,
+ * packets per warp batch, lanes per (packet, segment) item in pass S, CTAs
+ * per SM the shared memory allows, and the shared-memory bytes per CTA.  All
+ * outputs are host ints (any may be NULL).  HAMMING_E_ARG for a bad shape or
+ * stride. */
+hamming_status hamming_packet_launch_shape(uint32_t msg_bytes, int t, uint64_t rx_stride, uint64_t n_packets,
+                                           int sm_count, int *warps, int *packets_per_batch, int *lanes_per_item,
+                                           int *ctas_per_sm, int *smem_bytes);
+
 hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void *rx_dev, uint64_t rx_stride,
                                       uint64_t n_packets, void *msg_dev, uint64_t msg_stride,
                                       uint16_t *syndromes_dev, uint8_t *status_dev,

@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
     L.hamming_packet_coded_bytes.restype = u64
     L.hamming_packet_layout.argtypes = [u32, c_int, vp, vp]
     L.hamming_packet_layout.restype = c_int
+    L.hamming_packet_launch_shape.argtypes = [u32, c_int, u64, u64, c_int, vp, vp, vp, vp, vp]
+    L.hamming_packet_launch_shape.restype = c_int
     L.hamming_decode_packets.argtypes = [u32, c_int, vp, u64, u64, vp, u64, vp, vp, vp, vp]
     L.hamming_decode_packets.restype = c_int
     L.hamming_encode_packets.argtypes = [u32, c_int, vp, u64, u64, vp, u64, vp]

@@ -250,6 +250,17 @@ def packet_stride(msg_bytes: int, t: int) -> int:
     return (packet_coded_bytes(msg_bytes, t) + 15) // 16 * 16
 
 
+def packet_launch_shape(msg_bytes: int, t: int, n_packets: int, rx_stride: Optional[int] = None,
+                        sm_count: int = 148) -> dict:
+    """The launch shape hamming_decode_packets picks (host-only query, no CUDA call)."""
+    rx_stride = packet_stride(msg_bytes, t) if rx_stride is None else rx_stride
+    vals = [ctypes.c_int(0) for _ in range(5)]
+    check(lib().hamming_packet_launch_shape(msg_bytes, t, rx_stride, int(n_packets), sm_count,
+                                            *[ctypes.byref(v) for v in vals]), "hamming_packet_launch_shape")
+    return dict(zip(("warps", "packets_per_batch", "lanes_per_item", "ctas_per_sm", "smem_bytes"),
+                    (v.value for v in vals)))
+
+
 @dataclass
 class PacketDecodeResult:
     messages: torch.Tensor             # uint8 [n_packets * msg_stride]

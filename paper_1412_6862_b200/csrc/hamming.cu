@@ -46,6 +46,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -2550,6 +2551,28 @@ hamming_status hamming_packet_layout(uint32_t msg_bytes, int t, uint32_t* seg_k,
     seg_k[i] = g.k[i];
     seg_n[i] = g.n[i];
   }
+  return HAMMING_OK;
+}
+
+hamming_status hamming_packet_launch_shape(uint32_t msg_bytes, int t, uint64_t rx_stride, uint64_t n_packets,
+                                           int sms, int* warps, int* G, int* L, int* ctas, int* smem) {
+  PacketGeom g;
+  hamming_status rc = packet_geom(msg_bytes, t, g);
+  if (rc != HAMMING_OK) return rc;
+  if (rx_stride % 16 != 0 || rx_stride < (g.coded_bits + 7) / 8)
+    return set_err(HAMMING_E_ARG, "hamming_packet_launch_shape: rx_stride must be a multiple of 16 >= the coded bytes");
+  PacketTables T;
+  rc = build_packet_tables(g, T);
+  if (rc != HAMMING_OK) return rc;
+  BatchGeom bg;
+  rc = batch_geom(g, T, rx_stride, std::min<uint64_t>(n_packets, 1ull << 31), sms, bg);
+  if (rc != HAMMING_OK) return rc;
+  const uint64_t bytes = bg.tab_bytes + static_cast<uint64_t>(bg.warps) * bg.warp_bytes;
+  if (warps) *warps = static_cast<int>(bg.warps);
+  if (G) *G = static_cast<int>(bg.G);
+  if (L) *L = static_cast<int>(bg.L);
+  if (ctas) *ctas = static_cast<int>(std::min<uint64_t>(228ull * 1024 / (bytes + 1536), 32 / bg.warps));
+  if (smem) *smem = static_cast<int>(bytes);
   return HAMMING_OK;
 }
 

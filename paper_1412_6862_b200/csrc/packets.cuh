@@ -408,86 +408,86 @@ struct BatchGeom {
   uint32_t tab_bytes;  // CTA tables in front of the warp areas
 };
 
-hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, BatchGeom& b) {
+hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, uint64_t n_packets, int sms,
+                          BatchGeom& b) {
   // a warp stages kPktStages whole strides: larger strides cannot be staged
   if (stride > (200u << 10) / kPktStages)
     return set_err(HAMMING_E_ARG, "packets: rx_stride too large to stage in shared memory (max 100 KiB)");
   uint32_t maxn = 0;
   for (uint32_t i = 0; i < g.t; ++i) maxn = max(maxn, g.n[i]);
-  // Launch shape, measured (tools/tune_shapes.py packets): the trade is warps per SM
-  // (latency hiding) against packets per batch (the per-batch costs -- TMA issue, bulk store,
-  // status, loop set-up -- amortised, and more bytes in flight per warp).  In order:
-  //   >= 6 packets with 12 warps x 9 KB (2 CTAs = 24 warps/SM)   M ~ 400
-  //   >= 4 packets with  8 warps x 13 KB (16 warps/SM)            M ~ 800
-  //   >= 2 packets with 12 warps x 9 KB                           M ~ 1200
-  //   else 16 warps x 6 KB (32 warps/SM, usually 1 packet)        M >= 1600
-  const uint64_t per = kPktStages * stride + kPktMsgBufs * 4ull * T.Wp + 4 + 4ull * g.t;
-  auto fit = [&](uint64_t budget) {
-    const uint64_t G = budget > 96 ? (budget - 96) / per : 1;
-    return std::max<uint64_t>(1, std::min<uint64_t>(G, 64));
+  constexpr uint64_t kSmemSM = 227ull * 1024;
+  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
+  // with head compaction (T.headx) the messages are written in place over the input stage: no
+  // message buffer
+  auto in_cap = [&](uint64_t G) { return 16 + G * stride + 16; };
+  auto msg_cap = [&](uint64_t G) { return T.headx ? 0ull : (G * T.Wp * 4 + 15) / 16 * 16 + 16; };
+  // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight),
+  // statuses and the boundary words of pass X
+  auto warp_bytes = [&](uint64_t G) {
+    return kPktStages * in_cap(G) + kPktMsgBufs * msg_cap(G) + 16 * ((G * 4 * (1 + g.t) + 15) / 16);
   };
-  uint64_t G;
-  if ((G = fit(9216)) >= 6) {
-    b.warps = 12;
-  } else if ((G = fit(13312)) >= 4) {
-    b.warps = 8;
-  } else if ((G = fit(9216)) >= 2) {
-    b.warps = 12;
-  } else {
-    G = fit(6144);
-    b.warps = 16;
-  }
-#ifdef HAM_PKT_BUDGET
-  G = fit(HAM_PKT_BUDGET);
-  b.warps = kPktWarps;
-#endif
-  // lanes per item in pass S: the L minimising an issue-count model of the pass --
-  // ceil(items / (32 / L)) rounds, each a fixed set-up + epilogue (~90 warp
-  // instructions, + 4 per shuffle step) and ceil(C64 / 4L) unrolled blocks of
-  // ~42 -- so short codewords and many items per batch take small groups.  The
-  // batch may also shrink (down to half the shape's G) when fewer packets fill
-  // the rounds better: the model's cost per packet counts ~150 more per batch.
+  // Launch shape by an issue model, over every warps-per-CTA w and packets-per-batch G
+  // that fit: per packet, pass S costs ceil(G t / (32 / L)) rounds of a fixed set-up + epilogue
+  // (~60 warp instructions with L >= 8, ~75 below) plus ceil(C64 / 4L) unrolled blocks of ~42 each,
+  // pass R ~14 (one packet per batch) or ~9.5 warp instructions per 32 message words, and every batch
+  // ~170 more; the issue rate falls off below 16 warps per SM as (W / 16)^0.7 (measured: 8 warps per
+  // SM lose ~25 % against 12, 24 gain ~20 % in issue but pay more per-batch work, profiles/
+  // r02_packets_tune.txt), and the last wave of batches counts as a whole wave.
   const uint32_t c64 = (maxn + 1) / 64 + 1;
-  auto best_L = [&](uint64_t Gc, uint32_t& L) {
-    const uint32_t items = static_cast<uint32_t>(Gc) * g.t;
-    uint64_t best = ~0ull;
-    for (uint32_t l = 1, lg = 0; l <= 32; l *= 2, ++lg) {
+  auto best_L = [&](uint64_t G, uint32_t& L) {
+    const uint32_t items = static_cast<uint32_t>(G) * g.t;
+    double best = 1e300;
+    for (uint32_t l = 1; l <= 32; l *= 2) {
       const uint64_t rounds = (items + 32 / l - 1) / (32 / l);
-      const uint64_t cost = rounds * (90 + 4 * (l == 32 ? 0 : lg) + 42 * ((c64 + 4 * l - 1) / (4 * l)));
+      const double cost = static_cast<double>(rounds) * ((l >= 8 ? 60.0 : 75.0) + 42.0 * ((c64 + 4 * l - 1) / (4 * l)));
       if (cost < best) best = cost, L = l;
     }
     return best;
   };
-  uint32_t L = 1;
-  {
-    uint64_t Gbest = G;
-    double score = 1e300;
-    for (uint64_t Gc = G; Gc >= 1 && 2 * Gc >= G; --Gc) {
-      uint32_t l = 1;
-      const double sc = static_cast<double>(best_L(Gc, l) + 150) / static_cast<double>(Gc);
-      if (sc < score * 0.999) score = sc, Gbest = Gc, L = l;
+  double score = 1e300;
+  b.warps = 0;
+  for (uint32_t w = 4; w <= static_cast<uint32_t>(kPktWarps); w += 2) {
+    for (uint64_t G = 1; G <= 64; ++G) {
+      const uint64_t smem = b.tab_bytes + w * warp_bytes(G);
+      if (smem > kSmemSM) break;
+      // 228 KB per SM, 1 KB reserved per CTA (+ the kernel's static tables); 64 registers per
+      // thread cap an SM at 32 warps
+      const uint64_t ctas = std::min<uint64_t>(228ull * 1024 / (smem + 1536), 32 / w);
+      if (ctas == 0) continue;
+      const double W = static_cast<double>(ctas * w);
+      uint32_t L = 1;
+      const double r_pp = (T.Wp / 32.0) * (G == 1 ? 14.0 : 9.5);
+      const double per_packet = (best_L(G, L) + 170.0) / static_cast<double>(G) + r_pp;
+      const double issue = std::pow(std::min(1.0, W / 16.0), 0.7);
+      const uint64_t batches = (n_packets + G - 1) / G, slots = static_cast<uint64_t>(std::max(1, sms)) * ctas * w;
+      const uint64_t waves = std::max<uint64_t>(1, (batches + slots - 1) / slots);
+      const double eff = static_cast<double>(batches) / static_cast<double>(waves * slots);
+      const double sc = per_packet / issue / std::max(eff, 1e-9);
+      if (sc < score * 0.999) score = sc, b.warps = w, b.G = static_cast<uint32_t>(G), b.L = L;
     }
-    G = Gbest;
   }
-  b.G = static_cast<uint32_t>(G);
+#ifdef HAM_PKT_BUDGET  // tuning builds: the pre-round-2 budget rule
+  {
+    const uint64_t per = kPktStages * stride + (T.headx ? 0ull : kPktMsgBufs * 4ull * T.Wp) + 4 + 4ull * g.t;
+    b.G = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((HAM_PKT_BUDGET - 96) / per, 64)));
+    b.warps = kPktWarps;
+    uint32_t L = 1;
+    best_L(b.G, L);
+    b.L = L;
+  }
+#endif
 #ifdef HAM_PKT_L
-  L = HAM_PKT_L;
+  b.L = HAM_PKT_L;
 #endif
 #ifdef HAM_PKT_TUNE  // tuning builds only: lanes per item from the environment
-  if (const char* e = getenv("HAM_PKT_L")) L = static_cast<uint32_t>(atoi(e));
+  if (const char* e = getenv("HAM_PKT_L")) b.L = static_cast<uint32_t>(atoi(e));
 #endif
-  b.L = L;
-  b.in_cap = static_cast<uint32_t>(16 + G * stride + 16);
-  b.msg_cap = static_cast<uint32_t>((G * T.Wp * 4 + 15) / 16 * 16 + 16);
-  // kPktStages input buffers (TMA prefetch depth), kPktMsgBufs message buffers (bulk stores in flight)
-  b.warp_bytes = kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
-                 static_cast<uint32_t>(16 * ((G * 4 * (1 + g.t) + 15) / 16));  // + statuses, item syndromes
-  b.tab_bytes = (16 * T.Wp + 8 * T.n_pieces + 8 * T.n_special + 4 * 7 * kPktMaxSeg + 15) / 16 * 16;
-  // a padded stride (any multiple of 16 >= the coded bytes is legal) can make the
-  // shape's warps overflow shared memory: fewer warps per CTA then (the kernel
-  // takes its warp count from blockDim)
-  while (b.warps > 1 && b.tab_bytes + static_cast<uint64_t>(b.warps) * b.warp_bytes > 227ull * 1024) --b.warps;
-  if (b.tab_bytes + static_cast<uint64_t>(b.warp_bytes) > 227ull * 1024)
+  if (b.warps == 0) return set_err(HAMMING_E_ARG, "packets: one packet (rx_stride) does not fit shared memory");
+  b.in_cap = static_cast<uint32_t>(in_cap(b.G));
+  b.msg_cap = static_cast<uint32_t>(msg_cap(b.G));
+  b.warp_bytes = static_cast<uint32_t>(warp_bytes(b.G));
+  while (b.warps > 1 && b.tab_bytes + static_cast<uint64_t>(b.warps) * b.warp_bytes > kSmemSM) --b.warps;
+  if (b.tab_bytes + static_cast<uint64_t>(b.warp_bytes) > kSmemSM)
     return set_err(HAMMING_E_ARG, "packets: one packet (rx_stride) does not fit shared memory");
   return HAMMING_OK;
 }
@@ -503,24 +503,37 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
 // the tail (positions 64 Jf .. n, at most two masked 32-bit chunks).
 template <uint32_t L>
 __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t off, uint32_t n, bool active,
-                                                     uint32_t q) {
+                                                     uint32_t q, uint32_t mq, uint32_t gid) {
   const uint32_t o = off + kPadBits - 1;
   const uint32_t rb = o & 31u;
-  const uint32_t full = active ? (n + 1) / 64 : 0;  // full 64-position chunks
+  const uint32_t np1 = active ? n + 1 : 0;  // positions 0 .. n
+  const uint32_t full = np1 / 64;           // full 64-position chunks
+  const uint32_t rest = np1 - 64 * full;    // positions of the partial chunk J = full (0 .. 63)
+  const uint32_t nch = full + (rest != 0 ? 1u : 0u);
+  // the partial chunk is a chunk like the others with the positions past n masked off: its
+  // 64 full par(Y) and 32 par(hi) terms are exactly the generic ones
+  const uint32_t mlo = __funnelshift_lc(0xFFFFFFFFu, 0u, rest);
+  const uint32_t mhi = __funnelshift_lc(0xFFFFFFFFu, 0u, rest > 32 ? rest - 32 : 0u);
   const uint32_t* wq = w + (o >> 5) + 2 * q;
   uint32_t X = 0, H = 0, A0 = 0, A1 = 0, BB = 0;
   // one block = 4 chunks per lane; blocks below full / 4L are complete for every lane of the
-  // group, so only the last, partial block tests which of its chunks exist
+  // group, so only the last block tests which of its chunks exist (and masks the partial one)
   auto block = [&](uint32_t blk, auto checked) {
     const uint32_t* wb = wq + 8 * L * blk;
-    const int cnt = static_cast<int>(full - 4 * L * blk) - static_cast<int>(q);
+    const int cnt = static_cast<int>(nch - 4 * L * blk) - static_cast<int>(q);
     uint32_t Xb = 0;
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       if (!decltype(checked)::value || static_cast<int>(L) * it < cnt) {
         const uint32_t w0 = wb[2 * L * it], w1 = wb[2 * L * it + 1], w2 = wb[2 * L * it + 2];
-        const uint32_t hi = __funnelshift_r(w1, w2, rb);
-        const uint32_t y = __funnelshift_r(w0, w1, rb) ^ hi;
+        uint32_t hi = __funnelshift_r(w1, w2, rb), lo = __funnelshift_r(w0, w1, rb);
+        if constexpr (decltype(checked)::value) {
+          if (rest != 0 && static_cast<int>(L) * it == cnt - 1) {  // chunk J = full
+            lo &= mlo;
+            hi &= mhi;
+          }
+        }
+        const uint32_t y = lo ^ hi;
         Xb ^= y;
         H ^= hi;
         if (it & 1) A0 ^= y;
@@ -532,18 +545,9 @@ __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t
   };
   const uint32_t nb = full / (4 * L);
   for (uint32_t blk = 0; blk < nb; ++blk) block(blk, std::false_type{});
-  if (4 * L * nb < full) block(nb, std::true_type{});
+  if (4 * L * nb < nch) block(nb, std::true_type{});
   uint32_t P = (64u * ((q * (__popc(X) & 1u)) ^ L * ((4u * BB) ^ (__popc(A0) & 1u) ^ ((__popc(A1) & 1u) << 1)))) ^
                (32u * (__popc(H) & 1u));
-  if (active && q == 0) {  // the tail: positions 64 full .. n (fewer than 64)
-    const uint32_t j = 2 * full, b0 = (o >> 5) + j;
-    const uint32_t rest = n + 1 - 64 * full;  // positions left, 0 .. 63
-    const uint32_t lo = __funnelshift_r(w[b0], w[b0 + 1], rb) & __funnelshift_lc(0xFFFFFFFFu, 0u, rest);
-    const uint32_t hi = __funnelshift_r(w[b0 + 1], w[b0 + 2], rb) &
-                        __funnelshift_lc(0xFFFFFFFFu, 0u, rest > 32 ? rest - 32 : 0u);
-    X ^= lo ^ hi;
-    P ^= ((__popc(lo) & 1u) ? 32u * j : 0u) ^ ((__popc(hi) & 1u) ? 32u * (j + 1) : 0u);
-  }
   if constexpr (L == 32) {
     X = __reduce_xor_sync(0xffffffffu, X);
     P = __reduce_xor_sync(0xffffffffu, P);
@@ -554,7 +558,19 @@ __device__ __forceinline__ uint32_t group_syndrome64(const uint32_t* w, uint32_t
       P ^= __shfl_xor_sync(0xffffffffu, P, sh);
     }
   }
-  return P ^ xor_of_indices(X);
+  if constexpr (L >= 8) {  // S5(X) by five lanes of the group at once: lane q < 5 holds bit q
+    const uint32_t bal = __ballot_sync(0xffffffffu, __popc(X & mq) & 1u);
+    return P ^ ((bal >> (gid * L)) & 31u);
+  } else {
+    return P ^ xor_of_indices(X);
+  }
+}
+
+// mask of the bit indices with bit q set (0xAAAAAAAA, 0xCCCCCCCC, ... 0xFFFF0000), 0 for q >= 5
+__device__ __forceinline__ uint32_t index_bit_mask(uint32_t q) {
+  if (q >= 5) return 0u;
+  const uint32_t h = 1u << q;
+  return (0xFFFFFFFFu / ((1u << h) + 1u)) << h;
 }
 
 // q = u / d, r = u % d from mag = floor(2^32 / d) (2^32 - 1 for d = 1): the
@@ -604,6 +620,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   }
   uint8_t* wb = smem + bg.tab_bytes + warp * bg.warp_bytes;
   uint32_t* pst = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + kPktMsgBufs * bg.msg_cap);  // statuses
+  uint32_t* bside = pst + bg.G;  // HX: the boundary message words of the batch's items, [packet][segment]
   uint64_t* bars = bars_all + warp * kPktStages;
   if (threadIdx.x < 2) cta_counts[threadIdx.x] = 0;
   __syncthreads();
@@ -616,8 +633,10 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   const uint64_t pol = policy_evict_first();
   const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
   const uint32_t groups = 32 / L;
+  const uint32_t mq = index_bit_mask(q);  // pass S, L >= 8: this lane's bit of S5
   const uint32_t stride_bits = static_cast<uint32_t>(a.in_stride * 8);
   const uint32_t in_stride = static_cast<uint32_t>(a.in_stride);
+  const uint32_t wstride = in_stride / 4;  // words from one packet's slot to the next
   uint32_t n_corr = 0, n_fail = 0;
   auto batch_bytes = [&](uint32_t b) -> uint32_t { return min(nP - b * bg.G, bg.G) * in_stride; };
   auto batch_src = [&](uint32_t b) { return a.in + static_cast<uint64_t>(b) * bg.G * in_stride; };
@@ -643,9 +662,16 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     const uint32_t* w = reinterpret_cast<const uint32_t*>(wb + buf * bg.in_cap);
     const uint32_t p0 = b * bg.G;
     const uint32_t np = min(nP - p0, bg.G);
-    uint32_t* mbuf = reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + (it % kPktMsgBufs) * bg.msg_cap);
+    // messages: with HX in place -- packet p's message words over the start of its own slot of
+    // the input stage (word W of a message never lands above the stream words it is built from,
+    // see pass R), so no message buffer; otherwise a separate buffer, packet pk at word pk * Wp
+    uint32_t* mbuf = HX ? const_cast<uint32_t*>(w) + 4
+                        : reinterpret_cast<uint32_t*>(wb + kPktStages * bg.in_cap + (it % kPktMsgBufs) * bg.msg_cap);
+    const uint32_t mstride = HX ? wstride : Wp;  // words from one packet's message to the next
     uint16_t* syn_b = a.syn != nullptr ? a.syn + static_cast<uint64_t>(p0) * g.t : nullptr;
-    if (lane == 0) bulk_wait_read<kPktMsgBufs - 1>();  // the bulk store that last used this mbuf has read it
+    if constexpr (!HX) {
+      if (lane == 0) bulk_wait_read<kPktMsgBufs - 1>();  // the bulk store that last used this mbuf has read it
+    }
     // G <= 64: two predicated stores (a lane-strided loop here compiles to ~40 instructions of unroll set-up)
     if (static_cast<uint32_t>(lane) < np) pst[lane] = 0;
     if (static_cast<uint32_t>(lane) + 32 < np) pst[lane + 32] = 0;
@@ -664,7 +690,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         const uint32_t pk = divmod_small(active ? base + gid : 0, g.t, T.mag_t, seg);
         const uint32_t n = active ? sg[kPktMaxSeg + seg] : 0;
         const uint32_t off = pk * stride_bits + sg[seg];
-        const uint32_t s = group_syndrome64<L>(w, off, n, active, q);
+        const uint32_t s = group_syndrome64<L>(w, off, n, active, q, mq, gid);
         // every lane's loads of this round are done (the group reduction above is warp-synchronous):
         // flipping a bit of this item cannot race with another item's reads, whose chunks never
         // count a bit outside their own positions 0..n
@@ -712,19 +738,30 @@ __global__ void __launch_bounds__(kPktWarps * 32)
               const uint32_t m0 = __funnelshift_lc(0xFFFFFFFFu, 0u, nb0);
               const uint32_t tail = ((__funnelshift_r(a0, a1, s0) & m0) | (__funnelshift_rc(a0, a1, (s0 & 31u) + 1) & ~m0)) &
                                     __funnelshift_lc(0xFFFFFFFFu, 0u, lt);
-              mbuf[pk * Wp + W] = tail | (d0 << lt);
+              bside[pk * g.t + seg] = tail | (d0 << lt);  // written into place after pass R
             }
           }
         }
       }
     }
     __syncwarp();
+    if constexpr (HX) {  // refill the previous stage once its in-place bulk stores have read it
+      if (it > 0) {
+        bulk_wait_read<0>();  // every lane: the stores it issued for the previous batch
+        __syncwarp();
+        const uint32_t nx = b + (kPktStages - 1) * nw;
+        const uint32_t ps = (it + kPktStages - 1) % kPktStages;
+        if (lane == 0 && nx < n_batches) {
+          mbar_arrive_expect_tx(&bars[ps], batch_bytes(nx));
+          bulk_g2s(wb + ps * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[ps], pol);
+        }
+      }
+    }
     {  // pass R: every word as one or two slices (lane: word W of every packet of the batch).
        // Loads are issued kRU words (or packets) at a time before any store, so a
        // warp has kRU independent shared-memory round trips in flight instead of one
        // (the stores go to the message buffer, which no load of this pass reads).
       constexpr uint32_t kRU = kPktRU;
-      const uint32_t wstride = static_cast<uint32_t>(a.in_stride / 4);
       // slice 1 is the stream one bit further on (the parity position skipped)
       auto rr = [](uint32_t a0, uint32_t a1, const uint4& d) {
         return (__funnelshift_r(a0, a1, d.y) & d.z) | (__funnelshift_rc(a0, a1, d.w) & ~d.z);
@@ -753,17 +790,17 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];  // {word, shift, mask of slice 0, shift + 1 (0: head word)}
           if (d.w == 0) continue;    // a head word: pass X (or H) writes it
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
-          uint32_t* mp = mbuf + W;
-          uint32_t p = 0;
-          for (; p + kRU <= np; p += kRU, wp += kRU * wstride, mp += kRU * Wp) {
+          uint32_t* mp = mbuf + W;  // packet p's word W at mbuf + p * mstride
+          // kRU packets per step, the last step predicated (np is 2 .. G)
+          for (uint32_t p = 0; p < np; p += kRU, wp += kRU * wstride, mp += kRU * mstride) {
             uint32_t x0[kRU], x1[kRU];
 #pragma unroll
-            for (uint32_t u = 0; u < kRU; ++u) x0[u] = wp[u * wstride], x1[u] = wp[u * wstride + 1];
+            for (uint32_t u = 0; u < kRU; ++u)
+              if (p + u < np) x0[u] = wp[u * wstride], x1[u] = wp[u * wstride + 1];
 #pragma unroll
-            for (uint32_t u = 0; u < kRU; ++u) mp[u * Wp] = rr(x0[u], x1[u], d);
+            for (uint32_t u = 0; u < kRU; ++u)
+              if (p + u < np) mp[u * mstride] = rr(x0[u], x1[u], d);
           }
-#pragma unroll 1
-          for (; p < np; ++p, wp += wstride, mp += Wp) *mp = rr(wp[0], wp[1], d);
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
         #pragma unroll 1
@@ -774,7 +811,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           const uint4 d = wdesc[W];
           const uint32_t* wp = w + 4 + d.x + p * wstride;
           const uint32_t a0 = wp[0], a1 = wp[1];
-          if (d.w) mbuf[p * Wp + W] = rr(a0, a1, d);
+          if (d.w) mbuf[p * mstride + W] = rr(a0, a1, d);
         }
       }
     }
@@ -798,32 +835,49 @@ __global__ void __launch_bounds__(kPktWarps * 32)
       }
     }
     __syncwarp();
-    if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
-      const uint32_t nx = b + kPktStages * nw;
-      if (nx < n_batches) {
-        mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
-        bulk_g2s(wb + buf * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[buf], pol);
+    if constexpr (HX) {  // the boundary words pass X assembled, now that pass R has read the stream
+      __syncwarp();
+#pragma unroll 1
+      for (uint32_t e = lane; e < np * g.t; e += 32) {
+        uint32_t seg;
+        const uint32_t p = divmod_small(e, g.t, T.mag_t, seg);
+        const uint32_t W = sg[4 * kPktMaxSeg + seg];
+        if (W != 0xFFFFFFFFu) mbuf[p * mstride + W] = bside[e];
+      }
+    } else {
+      if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
+        const uint32_t nx = b + kPktStages * nw;
+        if (nx < n_batches) {
+          mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
+          bulk_g2s(wb + buf * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[buf], pol);
+        }
       }
     }
-    // write the batch's messages (packet pk at word pk * Wp of mbuf) and statuses
+    // write the batch's messages (packet pk at word pk * mstride of mbuf) and statuses
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
     const uintptr_t ob = reinterpret_cast<uintptr_t>(a.out + static_cast<uint64_t>(p0) * a.out_stride);
     if (bulk_out) {
       fence_proxy_async_smem();  // this lane's st.shared / atomics visible to the bulk copy
       __syncwarp();
-      if (lane == 0) {
+      if constexpr (HX) {  // one bulk store per packet, from its slot, issued by lane p
+        for (uint32_t pk = lane; pk < np; pk += 32)
+          bulk_s2g(reinterpret_cast<void*>(ob + pk * g.msg_bytes), mbuf + pk * mstride, g.msg_bytes, pol);
+        bulk_commit();
+      } else if (lane == 0) {
         bulk_s2g(reinterpret_cast<void*>(ob), mbuf, np * g.msg_bytes, pol);
         bulk_commit();
       }
     } else if ((g.msg_bytes & 3u) == 0 && (a.out_stride & 3u) == 0 && (ob & 3u) == 0) {
+      __syncwarp();
       for (uint32_t pk = 0; pk < np; ++pk) {
         uint32_t* dst = reinterpret_cast<uint32_t*>(ob + pk * a.out_stride);
-        for (uint32_t i = lane; i < Wp; i += 32) dst[i] = mbuf[pk * Wp + i];
+        for (uint32_t i = lane; i < Wp; i += 32) dst[i] = mbuf[pk * mstride + i];
       }
     } else {
+      __syncwarp();
       for (uint32_t pk = 0; pk < np; ++pk) {
         uint8_t* dst = reinterpret_cast<uint8_t*>(ob + pk * a.out_stride);
-        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * Wp * 4 + i];
+        for (uint32_t i = lane; i < g.msg_bytes; i += 32) dst[i] = mb[pk * mstride * 4 + i];
       }
     }
     if (a.status != nullptr) {
@@ -832,7 +886,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     }
     __syncwarp();
   }
-  if (lane == 0) bulk_wait<0>();  // the last bulk stores have completed before shared memory goes away
+  bulk_wait<0>();  // every lane: its last bulk stores have completed before shared memory goes away
   if (a.counts != nullptr) {
     n_corr = __reduce_add_sync(0xffffffffu, n_corr);
     n_fail = __reduce_add_sync(0xffffffffu, n_fail);
@@ -859,7 +913,9 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
     T_t = g.t;
   }
   BatchGeom bg;
-  hamming_status rc = batch_geom(g, T, a.in_stride, bg);
+  int dev0 = 0;
+  if (cudaGetDevice(&dev0) != cudaSuccess) dev0 = 0;
+  hamming_status rc = batch_geom(g, T, a.in_stride, std::min<uint64_t>(a.n_packets, 1ull << 31), sm_count(dev0), bg);
   if (rc != HAMMING_OK) return rc;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1045,6 +1101,9 @@ __global__ void __launch_bounds__(WARPS * 32)
     perfect_long_kernel(const __grid_constant__ LongArgs a) {
   using G = LongGeo<M>;
   constexpr uint32_t IN_B = G::IN_BYTES, OUT_B = G::OUT_BYTES, SYN_B = G::B;
+  // two input buffers (TMA prefetch), one output buffer {data, syndromes}: measured, a second
+  // output buffer (no wait for the previous batch's store) costs more in warps per SM than the
+  // wait does ((127,120) 0.94 -> 0.86, round 2)
   constexpr uint32_t WARP_BYTES = 2 * IN_B + OUT_B + SYN_B;  // every part a multiple of 16 bytes
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned long long cta_count;
@@ -1052,8 +1111,6 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31u;
   uint8_t* wb = smem + warp * WARP_BYTES;
-  uint32_t* obuf = reinterpret_cast<uint32_t*>(wb + 2 * IN_B);
-  uint8_t* sbuf = wb + 2 * IN_B + OUT_B;
   uint64_t* bars = bars_all + warp * 2;
   if (threadIdx.x == 0) cta_count = 0;
   __syncthreads();
@@ -1082,6 +1139,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     uint8_t* ib = wb + buf * IN_B;
     const bool full = b < n_full;
     const uint32_t nvalid = full ? G::B : static_cast<uint32_t>(a.N - b * G::B);
+    uint32_t* obuf = reinterpret_cast<uint32_t*>(wb + 2 * IN_B);
+    uint8_t* sbuf = wb + 2 * IN_B + OUT_B;
     if (lane == 0) bulk_wait_read<0>();  // the previous batch's bulk stores have read obuf and sbuf
     if (full) {
       mbar_wait(&bars[buf], (it >> 1) & 1u);

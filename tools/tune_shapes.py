@@ -37,7 +37,8 @@ M3_VARIANTS = [("DecodeLut3Op", 16, 12), ("DecodeLut3Op", 32, 6), ("DecodeLut3Op
                ("DecodeLut3PairOp", 24, 6)]
 # (63,57) decode and the probe ops (-DHAM_PROBE) at several shapes, for the sustained power probe
 POWER6_VARIANTS = [(8, 3, 0, 0), (8, 3, 1, 100000), (8, 3, 1, 2000), (8, 3, 2, 32), (8, 3, 2, 256), (8, 3, 2, 1000)]
-PKT_VARIANTS = [(6144, 2, 1, 16), (9216, 2, 1, 12), (12416, 2, 1, 8), (12416, 2, 1, 16), (18560, 2, 1, 8), (18560, 2, 1, 12), (24704, 2, 1, 8)]
+LONG_VARIANTS = [(16, 6), (12, 4), (8, 3)]  # (warps for m = 7, warps for m = 8)
+PKT_VARIANTS = [(9216, 2, 1, 12), (12416, 2, 1, 8), (14464, 2, 1, 14), (16512, 2, 1, 8), (18560, 2, 1, 12), (20608, 2, 1, 10), (24704, 2, 1, 8), (28800, 2, 1, 7)]
 
 
 def name(m, v):
@@ -76,6 +77,9 @@ def build():
         jobs = [(os.path.join(OUT, f"pw6_w{w}_s{st}_m{md}_{ns}.so"),
                  ["HAM_PROBE", f"HAM_W6={w}", f"HAM_S6={st}", f"HAM_WAIT_MODE={md}", f"HAM_WAIT_NS={ns}"])
                 for w, st, md, ns in POWER6_VARIANTS]
+    if len(sys.argv) > 2 and sys.argv[2] == "long":
+        jobs = [(os.path.join(OUT, f"long_w{w7}_{w8}.so"), [f"HAM_LONG_W7={w7}", f"HAM_LONG_W8={w8}"])
+                for w7, w8 in LONG_VARIANTS]
     if len(sys.argv) > 2 and sys.argv[2] == "m3":
         jobs = [(os.path.join(OUT, f"m3_{op}_w{w}_s{st}.so"), [f"HAM_M3_OP={op}", f"HAM_W3={w}", f"HAM_S3={st}"])
                 for op, w, st in M3_VARIANTS]
@@ -106,6 +110,12 @@ def run():
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "power_probe.py"), "--probe", "--only6",
                             "--no-copy"], env=env)
         return
+    if len(sys.argv) > 2 and sys.argv[2] == "long":
+        for w7, w8 in LONG_VARIANTS:
+            env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"long_w{w7}_{w8}.so"))
+            subprocess.run([sys.executable, os.path.join(ROOT, "tools", "quick_bench.py"), "--m", "7", "8",
+                            "--tag", f"w{w7}_{w8}"], env=env)
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "m3":
         for op, w, st in M3_VARIANTS:
             env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"m3_{op}_w{w}_s{st}.so"))
@@ -118,7 +128,7 @@ def run():
             env = dict(os.environ, HAMMING_LIB=os.path.join(OUT, f"pkt_{b}_{st}_{mb}_{w}.so"))
             print("budget", b, "stages", st, "msgbufs", mb, "warps", w, flush=True)
             subprocess.run([sys.executable, os.path.join(ROOT, "tools", "packets_bench.py"), "--M", "400", "800", "1200", "1600",
-                            "2000", "--t", "2", "5"], env=env)
+                            "2000", "--t", "2", "3", "5", "6"], env=env)
         return
     for m, vs in VARIANTS.items():
         for v in vs:
