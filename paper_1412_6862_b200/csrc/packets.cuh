@@ -585,6 +585,19 @@ __device__ __forceinline__ uint32_t divmod_small(uint32_t u, uint32_t d, uint32_
   return q;
 }
 
+// Pass R for U packets of one message word (descriptor d): all 2U loads first, then the U stores
+// (the message words land in the input stage, below every stream word still to be read).
+template <uint32_t U>
+__device__ __forceinline__ void rr_step(const uint32_t* wp, uint32_t* mp, const uint4& d, uint32_t wstride,
+                                        uint32_t mstride) {
+  uint32_t x0[U], x1[U];
+#pragma unroll
+  for (uint32_t u = 0; u < U; ++u) x0[u] = wp[u * wstride], x1[u] = wp[u * wstride + 1];
+#pragma unroll
+  for (uint32_t u = 0; u < U; ++u)
+    mp[u * mstride] = (__funnelshift_r(x0[u], x1[u], d.y) & d.z) | (__funnelshift_rc(x0[u], x1[u], d.w) & ~d.z);
+}
+
 template <uint32_t L, bool HX>
 __global__ void __launch_bounds__(kPktWarps * 32)
     packets_decode_kernel(const __grid_constant__ PacketGeom g, const __grid_constant__ BatchGeom bg,
@@ -791,15 +804,16 @@ __global__ void __launch_bounds__(kPktWarps * 32)
           if (d.w == 0) continue;    // a head word: pass X (or H) writes it
           const uint32_t* wp = w + 4 + d.x;  // (after the 16-byte pad)
           uint32_t* mp = mbuf + W;  // packet p's word W at mbuf + p * mstride
-          // kRU packets per step, the last step predicated (np is 2 .. G)
-          for (uint32_t p = 0; p < np; p += kRU, wp += kRU * wstride, mp += kRU * mstride) {
-            uint32_t x0[kRU], x1[kRU];
-#pragma unroll
-            for (uint32_t u = 0; u < kRU; ++u)
-              if (p + u < np) x0[u] = wp[u * wstride], x1[u] = wp[u * wstride + 1];
-#pragma unroll
-            for (uint32_t u = 0; u < kRU; ++u)
-              if (p + u < np) mp[u * mstride] = rr(x0[u], x1[u], d);
+          // kRU packets per step, then one exact step of the rest (no predicated-off slots: the
+          // compiler would otherwise issue every slot of a wide unrolled step for np = 2 .. 3)
+          uint32_t p = 0;
+#pragma unroll 1
+          for (; p + kRU <= np; p += kRU, wp += kRU * wstride, mp += kRU * mstride) rr_step<kRU>(wp, mp, d, wstride, mstride);
+          switch (np - p) {
+            case 3: rr_step<3>(wp, mp, d, wstride, mstride); break;
+            case 2: rr_step<2>(wp, mp, d, wstride, mstride); break;
+            case 1: rr_step<1>(wp, mp, d, wstride, mstride); break;
+            default: break;
           }
         }
         // the last Wp mod 32 words of every packet, flattened over (packet, word)
