@@ -166,3 +166,21 @@ def test_many_packets_multi_round(oracle, M, t):
         wm, ws, wst = oracle.decode_packets(M, t, rx_np[p0 * stride:(p0 + cnt) * stride], cnt, stride)
         assert np.array_equal(msgs[p0 * M:(p0 + cnt) * M], wm)
         assert np.array_equal(syn[p0:p0 + cnt].reshape(-1), ws.reshape(-1))
+
+
+@pytest.mark.parametrize("M,t,msg_stride", [(1200, 3, 1216), (1201, 5, 1201), (400, 6, 404), (2000, 2, 4096)])
+def test_in_place_messages_with_word_and_byte_stores(M, t, msg_stride):
+    """The head-compacted path writes messages in place over the input stage and
+    refills a stage only after its stores have read it.  With a strided or
+    unaligned message layout the stores are lane stores instead of TMA bulk
+    stores: many batches per warp, every message back as sent, the gap bytes
+    between strided messages untouched."""
+    P = 30_000
+    rx, sent = ham.packet_channel_generate(M, t, 0xBEE, 0, P, p=1.0, want_messages=True)
+    out = torch.full((P * msg_stride,), 0xA5, dtype=torch.uint8, device="cuda")
+    res = ham.decode_packets(M, t, rx, P, msg_out=out, msg_stride=msg_stride)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(P, msg_stride)
+    assert np.array_equal(o[:, :M].reshape(-1), sent.cpu().numpy()[: P * M])
+    assert (o[:, M:] == 0xA5).all()
+    assert res.counts.cpu().tolist() == [P * t, 0] and bool((res.status[:P] == 1).all())
