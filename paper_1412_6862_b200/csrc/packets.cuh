@@ -406,6 +406,9 @@ struct BatchGeom {
   uint32_t msg_cap;    // bytes of the message buffer: G packets of Wp words (+ slack)
   uint32_t warp_bytes; // 2*in_cap + msg_cap + status words
   uint32_t tab_bytes;  // CTA tables in front of the warp areas
+  uint32_t slot_words; // shared-memory words from one staged packet to the next (>= rx_stride / 4)
+  uint32_t copy_bytes; // 0: a batch is one TMA copy of G strides; else one copy of this many bytes per
+                       // packet into its slot (restaged at slot_words to spread pass S over the banks)
 };
 
 hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t stride, uint64_t n_packets, int sms,
@@ -479,13 +482,59 @@ hamming_status batch_geom(const PacketGeom& g, const PacketTables& T, uint64_t s
 #ifdef HAM_PKT_L
   b.L = HAM_PKT_L;
 #endif
+#ifdef HAM_PKT_TUNE  // tuning builds only: warps per CTA and packets per batch from the environment
+  if (const char* e = getenv("HAM_PKT_W")) b.warps = static_cast<uint32_t>(atoi(e));
+  if (const char* e = getenv("HAM_PKT_G")) {
+    b.G = static_cast<uint32_t>(atoi(e));
+    uint32_t L = 1;
+    best_L(b.G, L);
+    b.L = L;
+  }
+#endif
 #ifdef HAM_PKT_TUNE  // tuning builds only: lanes per item from the environment
   if (const char* e = getenv("HAM_PKT_L")) b.L = static_cast<uint32_t>(atoi(e));
 #endif
   if (b.warps == 0) return set_err(HAMMING_E_ARG, "packets: one packet (rx_stride) does not fit shared memory");
-  b.in_cap = static_cast<uint32_t>(in_cap(b.G));
+  // Pass S reads 32 / L items at once at unrelated offsets; with the packets at their global stride
+  // the same segment of packets p and p + 4 (any stride = 8 mod 32 words, e.g. M = 400) shares a
+  // bank.  Restage the batch at slot_words = 4 (stride / 16 + j), j < 8 (TMA needs 16-byte slots),
+  // choosing the j whose first round puts the fewest lanes on one bank (ties: the smallest j; j = 0
+  // keeps the single TMA copy per batch).
+  b.slot_words = static_cast<uint32_t>(stride / 4);
+  b.copy_bytes = 0;
+  {
+    auto worst = [&](uint32_t sw) {
+      uint32_t cnt[32] = {0}, mx = 0;
+      const uint32_t items = std::min<uint32_t>(b.G * g.t, 32 / b.L);
+      for (uint32_t it = 0; it < items; ++it) {
+        const uint32_t pk = it / g.t, seg = it % g.t;
+        const uint32_t base = (pk * sw * 32 + g.off[seg] + kPadBits - 1) >> 5;
+        for (uint32_t q = 0; q < b.L; ++q) mx = std::max(mx, ++cnt[(base + 2 * q) & 31u]);
+      }
+      return mx;
+    };
+    uint32_t best_sw = b.slot_words, best = worst(b.slot_words);
+    const uint32_t copy = (g.coded_bits + 7) / 8 + 15 - ((g.coded_bits + 7) / 8 + 15) % 16;  // coded bytes, to 16
+    for (uint32_t j = 1; j < 8 && b.G > 1; ++j) {
+      const uint32_t sw = static_cast<uint32_t>(stride / 4) + 4 * j;
+      const uint32_t wv = worst(sw);
+      if (wv < best) best = wv, best_sw = sw;
+    }
+    // only if the larger slots keep the CTAs per SM the shape was chosen with
+    auto ctas_at = [&](uint32_t sw) {
+      const uint64_t ic = 16 + static_cast<uint64_t>(b.G) * sw * 4 + 16;
+      const uint64_t wbytes = kPktStages * ic + kPktMsgBufs * msg_cap(b.G) + 16 * ((b.G * 4ull * (1 + g.t) + 15) / 16);
+      return 228ull * 1024 / (b.tab_bytes + b.warps * wbytes + 1536);
+    };
+    if (best_sw != b.slot_words && ctas_at(best_sw) >= ctas_at(b.slot_words)) {
+      b.slot_words = best_sw;
+      b.copy_bytes = copy;
+    }
+  }
+  b.in_cap = static_cast<uint32_t>(16 + static_cast<uint64_t>(b.G) * b.slot_words * 4 + 16);
   b.msg_cap = static_cast<uint32_t>(msg_cap(b.G));
-  b.warp_bytes = static_cast<uint32_t>(warp_bytes(b.G));
+  b.warp_bytes = static_cast<uint32_t>(kPktStages * b.in_cap + kPktMsgBufs * b.msg_cap +
+                                       16 * ((static_cast<uint64_t>(b.G) * 4 * (1 + g.t) + 15) / 16));
   while (b.warps > 1 && b.tab_bytes + static_cast<uint64_t>(b.warps) * b.warp_bytes > kSmemSM) --b.warps;
   if (b.tab_bytes + static_cast<uint64_t>(b.warp_bytes) > kSmemSM)
     return set_err(HAMMING_E_ARG, "packets: one packet (rx_stride) does not fit shared memory");
@@ -647,23 +696,35 @@ __global__ void __launch_bounds__(kPktWarps * 32)
   const uint32_t q = static_cast<uint32_t>(lane) & (L - 1), gid = static_cast<uint32_t>(lane) / L;
   const uint32_t groups = 32 / L;
   const uint32_t mq = index_bit_mask(q);  // pass S, L >= 8: this lane's bit of S5
-  const uint32_t stride_bits = static_cast<uint32_t>(a.in_stride * 8);
   const uint32_t in_stride = static_cast<uint32_t>(a.in_stride);
-  const uint32_t wstride = in_stride / 4;  // words from one packet's slot to the next
+  const uint32_t wstride = bg.slot_words;  // shared-memory words from one packet's slot to the next
+  const uint32_t stride_bits = wstride * 32;
   uint32_t n_corr = 0, n_fail = 0;
-  auto batch_bytes = [&](uint32_t b) -> uint32_t { return min(nP - b * bg.G, bg.G) * in_stride; };
-  auto batch_src = [&](uint32_t b) { return a.in + static_cast<uint64_t>(b) * bg.G * in_stride; };
+  // stage batch b into stage s (warp-uniform call): one TMA copy of the batch's strides, or with
+  // restaging one copy per packet into its slot, issued by lane p (lane 0 arms the barrier first)
+  auto load_batch = [&](uint32_t s, uint32_t b) {
+    const uint32_t npb = min(nP - b * bg.G, bg.G);
+    const uint8_t* src = a.in + static_cast<uint64_t>(b) * bg.G * in_stride;
+    uint8_t* dst = wb + s * bg.in_cap + 16;
+    if (bg.copy_bytes == 0) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bars[s], npb * in_stride);
+        bulk_g2s(dst, src, npb * in_stride, &bars[s], pol);
+      }
+    } else {
+      if (lane == 0) mbar_arrive_expect_tx(&bars[s], npb * bg.copy_bytes);
+      __syncwarp();
+      for (uint32_t p = lane; p < npb; p += 32)
+        bulk_g2s(dst + p * wstride * 4, src + p * in_stride, bg.copy_bytes, &bars[s], pol);
+    }
+  };
   if (lane == 0) {
     for (uint32_t s = 0; s < kPktStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    for (uint32_t s = 0; s < kPktStages; ++s) {
-      const uint32_t b = gw + s * nw;
-      if (b < n_batches) {
-        mbar_arrive_expect_tx(&bars[s], batch_bytes(b));
-        bulk_g2s(wb + s * bg.in_cap + 16, batch_src(b), batch_bytes(b), &bars[s], pol);
-      }
-    }
   }
+  __syncwarp();
+  for (uint32_t s = 0; s < kPktStages; ++s)
+    if (gw + s * nw < n_batches) load_batch(s, gw + s * nw);
   __syncwarp();
   // contiguous 16-byte-aligned messages leave by one TMA bulk store per batch (decided once:
   // with msg_bytes a multiple of 16 every batch's start stays aligned)
@@ -764,10 +825,7 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         __syncwarp();
         const uint32_t nx = b + (kPktStages - 1) * nw;
         const uint32_t ps = (it + kPktStages - 1) % kPktStages;
-        if (lane == 0 && nx < n_batches) {
-          mbar_arrive_expect_tx(&bars[ps], batch_bytes(nx));
-          bulk_g2s(wb + ps * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[ps], pol);
-        }
+        if (nx < n_batches) load_batch(ps, nx);
       }
     }
     {  // pass R: every word as one or two slices (lane: word W of every packet of the batch).
@@ -859,13 +917,8 @@ __global__ void __launch_bounds__(kPktWarps * 32)
         if (W != 0xFFFFFFFFu) mbuf[p * mstride + W] = bside[e];
       }
     } else {
-      if (lane == 0) {  // buffer consumed: prefetch the batch two steps ahead
-        const uint32_t nx = b + kPktStages * nw;
-        if (nx < n_batches) {
-          mbar_arrive_expect_tx(&bars[buf], batch_bytes(nx));
-          bulk_g2s(wb + buf * bg.in_cap + 16, batch_src(nx), batch_bytes(nx), &bars[buf], pol);
-        }
-      }
+      const uint32_t nx = b + kPktStages * nw;  // buffer consumed: prefetch the batch two steps ahead
+      if (nx < n_batches) load_batch(buf, nx);
     }
     // write the batch's messages (packet pk at word pk * mstride of mbuf) and statuses
     const uint8_t* mb = reinterpret_cast<const uint8_t*>(mbuf);
