@@ -572,12 +572,12 @@ def run_sweeps(ham, torch, dev, peak):
         cold, warm = [], []
         for _ in range(reps):
             flush.zero_()
-            torch.cuda._sleep(20000)  # keep the stream busy while the host enqueues the call
+            torch.cuda._sleep(200000)  # ~100 us: longer than the host needs to enqueue the call
             a, b = ev(), ev()
             a.record(st)
             ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
             b.record(st)
-            torch.cuda._sleep(20000)
+            torch.cuda._sleep(200000)
             a2, b2 = ev(), ev()
             a2.record(st)
             ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
