@@ -2015,6 +2015,97 @@ bool bits_overflow(int m, uint64_t N) {
 // Below this many codewords a call uses the light small-packet launch.
 constexpr uint64_t kSmallPacketCw = 1u << 16;
 
+// Small calls (at most kSmallCallBits coded bits, e.g. the BJ configs[0] 4 KB packet): the tile
+// pipeline gives every lane 32 consecutive codewords, so a 4 KB (7,4) packet keeps ~150 lanes busy
+// for 32 dependent decodes each and a call costs ~10 us of device time (ncu: 3065 warp instructions
+// in 12.7 us on one SM).  Instead one CTA of 1024 threads stages the stream in shared memory with
+// coalesced 16-byte loads, then decodes one codeword per thread at a time (a2..a4 as decode_cw),
+// gathers the data bits with shared atomics, writes whole words, syndromes and the count once.
+constexpr uint64_t kSmallCallBits = 1u << 17;  // 16 KiB of coded stream
+constexpr int kSmallCallThreads = 1024;
+
+template <int M>
+__global__ void __launch_bounds__(kSmallCallThreads)
+    small_decode_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ syn,
+                        uint32_t N, uint32_t in_bytes, uint32_t out_bytes, unsigned long long* __restrict__ counter,
+                        int accumulate) {
+  constexpr uint32_t n = Geo<M>::n, k = Geo<M>::k;
+  extern __shared__ __align__(16) uint32_t small_sm[];
+  __shared__ uint32_t cnt_s;
+  const uint32_t in_words = (in_bytes + 15) / 16 * 4 + 4;  // + a zero 16-byte unit: reads past the end
+  const uint32_t out_words = (N * k + 31) / 32;
+  uint32_t* sin = small_sm;
+  uint32_t* sout = small_sm + in_words;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t u = tid; u < in_words / 4; u += blockDim.x) {  // 16-byte units, zero past in_bytes
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (16 * u + 16 <= in_bytes) {
+      v = __ldg(reinterpret_cast<const uint4*>(in) + u);
+    } else if (16 * u < in_bytes) {
+      uint32_t wv[4] = {0, 0, 0, 0};
+      for (uint32_t b = 16 * u; b < in_bytes; ++b) wv[(b >> 2) & 3] |= static_cast<uint32_t>(in[b]) << (8 * (b & 3));
+      v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+    reinterpret_cast<uint4*>(sin)[u] = v;
+  }
+  for (uint32_t i = tid; i < out_words; i += blockDim.x) sout[i] = 0;
+  if (tid == 0) cnt_s = 0;
+  __syncthreads();
+  uint32_t cnt = 0;
+  for (uint32_t c = tid; c < N; c += blockDim.x) {
+    const uint32_t b = c * n, q = b >> 5, r = b & 31u;
+    const uint32_t lo = __funnelshift_r(sin[q], sin[q + 1], r);  // stream bits b .. b + 31
+    // v: bit p = position p (bit 0 a zero dummy); bits past n belong to the next codeword and are
+    // ignored by decode_cw's masks (m <= 5) or shifted out (m = 6)
+    uint32_t vlo = lo << 1, vhi = 0;
+    if constexpr (M == 6) vhi = (__funnelshift_r(sin[q + 1], sin[q + 2], r) << 1) | (lo >> 31);
+    uint32_t dlo, dhi;
+    const uint32_t s = decode_cw<M>(vlo, vhi, dlo, dhi);
+    const uint32_t P = c * k, pw = P >> 5, pr = P & 31u;
+    if constexpr (M <= 5) {
+      atomicOr(&sout[pw], dlo << pr);
+      if (pr + k > 32) atomicOr(&sout[pw + 1], dlo >> (32 - pr));
+    } else {
+      const uint64_t d = static_cast<uint64_t>(dlo) | (static_cast<uint64_t>(dhi) << 26);  // 57 bits
+      const uint64_t x = d << pr;
+      atomicOr(&sout[pw], static_cast<uint32_t>(x));
+      atomicOr(&sout[pw + 1], static_cast<uint32_t>(x >> 32));
+      if (pr + k > 64) atomicOr(&sout[pw + 2], static_cast<uint32_t>(d >> (64 - pr)));
+    }
+    if (syn != nullptr) syn[c] = static_cast<uint8_t>(s);
+    cnt += (s != 0);
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((tid & 31u) == 0 && cnt != 0) atomicAdd(&cnt_s, cnt);
+  __syncthreads();
+  for (uint32_t i = tid; i < out_words; i += blockDim.x) {  // only data bits were OR-ed in: pad bits are 0
+    const uint32_t v = sout[i];
+    if (4 * i + 4 <= out_bytes) {
+      reinterpret_cast<uint32_t*>(out)[i] = v;
+    } else {
+      for (uint32_t b = 4 * i; b < out_bytes; ++b) out[b] = static_cast<uint8_t>(v >> (8 * (b & 3)));
+    }
+  }
+  if (tid == 0) {
+    if (accumulate) atomicAdd(counter, static_cast<unsigned long long>(cnt_s));
+    else *counter = cnt_s;
+  }
+}
+
+template <int M>
+hamming_status launch_small_decode(const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
+                                   unsigned long long* counter, cudaStream_t st, bool accumulate) {
+  const uint32_t ib = static_cast<uint32_t>((Geo<M>::n * N + 7) / 8), ob = static_cast<uint32_t>((Geo<M>::k * N + 7) / 8);
+  const size_t smem = 4 * (((ib + 15) / 16 * 4 + 4) + (Geo<M>::k * N + 31) / 32);
+  small_decode_kernel<M><<<1, kSmallCallThreads, smem, st>>>(in, out, syn, static_cast<uint32_t>(N), ib, ob, counter,
+                                                              accumulate ? 1 : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "small decode launch");
+  g_launches = 1;
+  g_grid = 1;
+  return HAMMING_OK;
+}
+
 // Per-device build of the (15,11) table in global memory, once it succeeds: a
 // failed build (e.g. a first call made while the caller's stream is being
 // captured into a CUDA graph, where the build's own stream sync is not
@@ -2053,6 +2144,15 @@ hamming_status decode_dispatch(int m, const uint8_t* in, uint64_t N, uint8_t* ou
   if (m == 7 || m == 8) return launch_long_decode(m, in, N, out, syn, counter, st, accumulate);
   const uint64_t n = (1ull << m) - 1, k = n - m;
   const uint64_t ib = (n * N + 7) / 8, ob = (k * N + 7) / 8;
+  if (N > 0 && n * N <= kSmallCallBits) {  // a single small call: one CTA, no tile pipeline
+    switch (m) {
+      case 2: return launch_small_decode<2>(in, N, out, syn, counter, st, accumulate);
+      case 3: return launch_small_decode<3>(in, N, out, syn, counter, st, accumulate);
+      case 4: return launch_small_decode<4>(in, N, out, syn, counter, st, accumulate);
+      case 5: return launch_small_decode<5>(in, N, out, syn, counter, st, accumulate);
+      case 6: return launch_small_decode<6>(in, N, out, syn, counter, st, accumulate);
+    }
+  }
   if (N < kSmallPacketCw) {
     // Small packets are latency-bound: a light CTA (4 warps, 2 stages, no
     // table to build or copy) launches and finishes fastest; from 4 full tiles

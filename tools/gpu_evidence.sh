@@ -15,7 +15,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tile
   > $OUT/${TAG}_full_m6.log 2>&1
 for tool in initcheck memcheck; do
   echo "== $tool" >> $OUT/${TAG}_sanitizer.txt
-  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_workload.py \
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_workload.py $([ $tool = initcheck ] && echo --initcheck) \
     >> $OUT/${TAG}_sanitizer.txt 2>&1
   echo "rc=$?" >> $OUT/${TAG}_sanitizer.txt
 done
