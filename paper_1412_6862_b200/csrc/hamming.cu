@@ -2015,35 +2015,55 @@ bool bits_overflow(int m, uint64_t N) {
 // Below this many codewords a call uses the light small-packet launch.
 constexpr uint64_t kSmallPacketCw = 1u << 16;
 
-// Small calls (at most kSmallCallBits coded bits, e.g. the BJ configs[0] 4 KB packet): the tile
-// pipeline gives every lane 32 consecutive codewords, so a 4 KB (7,4) packet keeps ~150 lanes busy
-// for 32 dependent decodes each and a call costs ~10 us of device time (ncu: 3065 warp instructions
-// in 12.7 us on one SM).  Instead one CTA of 1024 threads stages the stream in shared memory with
-// coalesced 16-byte loads, then decodes one codeword per thread at a time (a2..a4 as decode_cw),
-// gathers the data bits with shared atomics, writes whole words, syndromes and the count once.
-constexpr uint64_t kSmallCallBits = 1u << 17;  // 16 KiB of coded stream
+// Small calls (at most kSmallCallBits coded bits, e.g. the BJ configs[0] 4 KB packet and the C2
+// sizes up to 512 KiB): the tile pipeline gives every lane 32 consecutive codewords, so a 4 KB (7,4)
+// packet kept ~150 lanes busy for 32 dependent decodes each and a call cost ~10 us of device time
+// (ncu: 3065 warp instructions in 12.7 us on one SM).  Instead CTAs of 1024 threads each take
+// small_call_cw<m>() consecutive codewords (a multiple of 32, so every CTA's input and output start on a
+// word), stage their stream in shared memory with coalesced 16-byte loads, decode one codeword per
+// thread at a time (a2..a4 as decode_cw), gather the data bits with shared atomics and write whole
+// words, the syndromes and the count.  One CTA writes the count itself; several publish it through
+// the stream's launch slot (the last CTA to finish writes it and resets the slot, as tiles_kernel)
+// or, without a slot (graph capture), add into a count zeroed by a memset first.
+constexpr uint64_t kSmallCallBits = 1u << 22;  // 512 KiB of coded stream
 constexpr int kSmallCallThreads = 1024;
+// codewords per CTA: the most (a multiple of 1024, at most 16384) whose stream and data images fit
+// the default 48 KB of shared memory -- 16384 for m = 2, 3 (BJ configs[0] is one CTA), 14336 for
+// m = 4, 6144 for m = 5, 3072 for m = 6
+template <int M>
+__host__ __device__ constexpr uint32_t small_call_cw() {
+  constexpr uint32_t bits = Geo<M>::n + Geo<M>::k;
+  uint32_t c = 16384;
+  while (c > 1024 && c * bits / 8 + 256 > 48 * 1024) c -= 1024;
+  return c;
+}
 
 template <int M>
 __global__ void __launch_bounds__(kSmallCallThreads)
     small_decode_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, uint8_t* __restrict__ syn,
-                        uint32_t N, uint32_t in_bytes, uint32_t out_bytes, unsigned long long* __restrict__ counter,
-                        int accumulate) {
+                        uint32_t N, uint32_t in_total, uint32_t out_total, unsigned long long* __restrict__ counter,
+                        int accumulate, LaunchSlot* __restrict__ slot, uint32_t CPB) {
   constexpr uint32_t n = Geo<M>::n, k = Geo<M>::k;
   extern __shared__ __align__(16) uint32_t small_sm[];
-  __shared__ uint32_t cnt_s;
+  __shared__ uint32_t cnt_s;  // 32-bit: a CTA holds at most 16384 codewords
+  const uint32_t c0 = blockIdx.x * CPB, nc = min(CPB, N - c0);
+  // this CTA's stream: bits [c0 n, (c0 + nc) n), byte ib0 = c0 n / 8 (a multiple of 4)
+  const uint32_t ib0 = c0 / 8 * n, in_bytes = min(in_total - ib0, (nc * n + 7) / 8 + 8);
+  const uint32_t ob0 = c0 / 8 * k, out_bytes = min(out_total - ob0, (nc * k + 7) / 8);
   const uint32_t in_words = (in_bytes + 15) / 16 * 4 + 4;  // + a zero 16-byte unit: reads past the end
-  const uint32_t out_words = (N * k + 31) / 32;
+  const uint32_t out_words = (nc * k + 31) / 32;
   uint32_t* sin = small_sm;
   uint32_t* sout = small_sm + in_words;
   const uint32_t tid = threadIdx.x;
+  const uint8_t* src = in + ib0;
   for (uint32_t u = tid; u < in_words / 4; u += blockDim.x) {  // 16-byte units, zero past in_bytes
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (16 * u + 16 <= in_bytes) {
-      v = __ldg(reinterpret_cast<const uint4*>(in) + u);
+    if (16 * u + 16 <= in_bytes && ((ib0 & 15u) == 0)) {
+      v = __ldg(reinterpret_cast<const uint4*>(src) + u);
     } else if (16 * u < in_bytes) {
       uint32_t wv[4] = {0, 0, 0, 0};
-      for (uint32_t b = 16 * u; b < in_bytes; ++b) wv[(b >> 2) & 3] |= static_cast<uint32_t>(in[b]) << (8 * (b & 3));
+      for (uint32_t b = 16 * u; b < in_bytes && b < 16 * u + 16; ++b)
+        wv[(b >> 2) & 3] |= static_cast<uint32_t>(src[b]) << (8 * (b & 3));
       v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
     reinterpret_cast<uint4*>(sin)[u] = v;
@@ -2052,12 +2072,13 @@ __global__ void __launch_bounds__(kSmallCallThreads)
   if (tid == 0) cnt_s = 0;
   __syncthreads();
   uint32_t cnt = 0;
-  for (uint32_t c = tid; c < N; c += blockDim.x) {
+  for (uint32_t c = tid; c < nc; c += blockDim.x) {
     const uint32_t b = c * n, q = b >> 5, r = b & 31u;
     const uint32_t lo = __funnelshift_r(sin[q], sin[q + 1], r);  // stream bits b .. b + 31
     // v: bit p = position p (bit 0 a zero dummy); bits past n belong to the next codeword and are
     // ignored by decode_cw's masks (m <= 5) or shifted out (m = 6)
-    uint32_t vlo = lo << 1, vhi = 0;
+    const uint32_t vlo = lo << 1;
+    uint32_t vhi = 0;
     if constexpr (M == 6) vhi = (__funnelshift_r(sin[q + 1], sin[q + 2], r) << 1) | (lo >> 31);
     uint32_t dlo, dhi;
     const uint32_t s = decode_cw<M>(vlo, vhi, dlo, dhi);
@@ -2072,23 +2093,40 @@ __global__ void __launch_bounds__(kSmallCallThreads)
       atomicOr(&sout[pw + 1], static_cast<uint32_t>(x >> 32));
       if (pr + k > 64) atomicOr(&sout[pw + 2], static_cast<uint32_t>(d >> (64 - pr)));
     }
-    if (syn != nullptr) syn[c] = static_cast<uint8_t>(s);
+    if (syn != nullptr) syn[c0 + c] = static_cast<uint8_t>(s);
     cnt += (s != 0);
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((tid & 31u) == 0 && cnt != 0) atomicAdd(&cnt_s, cnt);
   __syncthreads();
+  uint8_t* dst = out + ob0;
   for (uint32_t i = tid; i < out_words; i += blockDim.x) {  // only data bits were OR-ed in: pad bits are 0
     const uint32_t v = sout[i];
     if (4 * i + 4 <= out_bytes) {
-      reinterpret_cast<uint32_t*>(out)[i] = v;
+      reinterpret_cast<uint32_t*>(dst)[i] = v;
     } else {
-      for (uint32_t b = 4 * i; b < out_bytes; ++b) out[b] = static_cast<uint8_t>(v >> (8 * (b & 3)));
+      for (uint32_t b = 4 * i; b < out_bytes; ++b) dst[b] = static_cast<uint8_t>(v >> (8 * (b & 3)));
     }
   }
   if (tid == 0) {
-    if (accumulate) atomicAdd(counter, static_cast<unsigned long long>(cnt_s));
-    else *counter = cnt_s;
+    const unsigned long long cs = cnt_s;
+    if (gridDim.x == 1) {
+      if (accumulate) atomicAdd(counter, cs);
+      else *counter = cs;
+    } else if (slot != nullptr) {  // the last CTA to arrive publishes the total and resets the slot
+      if (cs) atomicAdd(&slot->sum[0], cs);
+      __threadfence();
+      if (atomicAdd(&slot->done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        const unsigned long long tot = atomicExch(&slot->sum[0], 0ull);
+        if (accumulate) atomicAdd(counter, tot);
+        else *counter = tot;
+        slot->claim = 0;
+        slot->done = 0;
+      }
+    } else if (cs) {  // count zeroed by the launcher (or accumulating)
+      atomicAdd(counter, cs);
+    }
   }
 }
 
@@ -2096,13 +2134,30 @@ template <int M>
 hamming_status launch_small_decode(const uint8_t* in, uint64_t N, uint8_t* out, uint8_t* syn,
                                    unsigned long long* counter, cudaStream_t st, bool accumulate) {
   const uint32_t ib = static_cast<uint32_t>((Geo<M>::n * N + 7) / 8), ob = static_cast<uint32_t>((Geo<M>::k * N + 7) / 8);
-  const size_t smem = 4 * (((ib + 15) / 16 * 4 + 4) + (Geo<M>::k * N + 31) / 32);
-  small_decode_kernel<M><<<1, kSmallCallThreads, smem, st>>>(in, out, syn, static_cast<uint32_t>(N), ib, ob, counter,
-                                                              accumulate ? 1 : 0);
+  // one CTA when the call fits one (no count to publish across CTAs); otherwise 2048 codewords per
+  // CTA, so that mid-size calls spread over many SMs (measured: 64 KiB of (15,11) in a CUDA graph
+  // 12.3 us with 3 CTAs of 14336 codewords, 8.2 us with 18 of 2048)
+  const uint32_t CPB = N <= small_call_cw<M>() ? static_cast<uint32_t>(N) : 2048u;
+  const uint32_t grid = static_cast<uint32_t>((N + CPB - 1) / CPB);
+  const uint32_t cpb = static_cast<uint32_t>(std::min<uint64_t>(N, CPB));
+  const size_t smem = 4 * (((Geo<M>::n * cpb + 7) / 8 + 8 + 15) / 16 * 4 + 4 + (Geo<M>::k * cpb + 31) / 32);
+  LaunchSlot* slot = nullptr;
+  if (grid > 1) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    slot = launch_slot(dev, st);
+    if (slot == nullptr && !accumulate) {  // no slot (graph capture): count zeroed first, then added
+      e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
+    }
+  }
+  small_decode_kernel<M><<<grid, kSmallCallThreads, smem, st>>>(in, out, syn, static_cast<uint32_t>(N), ib, ob, counter,
+                                                                 accumulate ? 1 : 0, slot, CPB);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "small decode launch");
   g_launches = 1;
-  g_grid = 1;
+  g_grid = static_cast<int>(grid);
   return HAMMING_OK;
 }
 
