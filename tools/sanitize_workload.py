@@ -2,8 +2,9 @@
 initcheck): every decode shape with ragged tails, encode, generate and the
 host pipeline, at sizes that keep the sanitizer fast.
 
---initcheck: the same kernels without the workload's own torch/cudaMemcpy
-copies of kernel outputs and without the host pipeline.  initcheck does not
+--initcheck: the same kernels on random received bytes written by a torch
+kernel, without the workload's own torch/cudaMemcpy copies of kernel outputs
+and without the host pipeline.  initcheck does not
 count bytes written by TMA bulk stores (cp.async.bulk) as initialised, so a
 cudaMemcpy that reads them is reported ("Uninitialized access ... by
 cudaMemcpy source", 12 472 such reports with the copies in, none from a kernel);
@@ -20,8 +21,11 @@ INIT = "--initcheck" in sys.argv
 
 for m in (2, 3, 4, 5, 6):
     for N in (1, 1023, 3 * 1024 + 77, 20_000):
-        exact = torch.empty(ham.coded_bytes(m, N), dtype=torch.uint8, device="cuda")
-        ham.channel_generate(m, 7, 0, N, p=0.3, q2=0.3, rx_out=exact)  # exactly the coded bytes
+        if INIT:  # written by a torch kernel (initcheck does not see TMA bulk stores as writes)
+            exact = torch.randint(0, 256, (ham.coded_bytes(m, N),), dtype=torch.uint8, device="cuda")
+        else:
+            exact = torch.empty(ham.coded_bytes(m, N), dtype=torch.uint8, device="cuda")
+            ham.channel_generate(m, 7, 0, N, p=0.3, q2=0.3, rx_out=exact)  # exactly the coded bytes
         res = ham.decode(m, exact, N)
         ham.decode(m, exact, N, syndromes=False)
         if INIT:
