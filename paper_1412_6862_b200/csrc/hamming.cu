@@ -2016,7 +2016,7 @@ bool bits_overflow(int m, uint64_t N) {
 constexpr uint64_t kSmallPacketCw = 1u << 16;
 
 // Small calls (at most kSmallCallBits coded bits, e.g. the BJ configs[0] 4 KB packet and the C2
-// sizes up to 512 KiB): the tile pipeline gives every lane 32 consecutive codewords, so a 4 KB (7,4)
+// sizes up to 2 MiB): the tile pipeline gives every lane 32 consecutive codewords, so a 4 KB (7,4)
 // packet kept ~150 lanes busy for 32 dependent decodes each and a call cost ~10 us of device time
 // (ncu: 3065 warp instructions in 12.7 us on one SM).  Instead CTAs of 1024 threads each take
 // small_call_cw<m>() consecutive codewords (a multiple of 32, so every CTA's input and output start on a
@@ -2025,7 +2025,7 @@ constexpr uint64_t kSmallPacketCw = 1u << 16;
 // words, the syndromes and the count.  One CTA writes the count itself; several publish it through
 // the stream's launch slot (the last CTA to finish writes it and resets the slot, as tiles_kernel)
 // or, without a slot (graph capture), add into a count zeroed by a memset first.
-constexpr uint64_t kSmallCallBits = 1u << 22;  // 512 KiB of coded stream
+constexpr uint64_t kSmallCallBits = 1u << 24;  // 2 MiB of coded stream
 constexpr int kSmallCallThreads = 1024;
 // codewords per CTA: the most (a multiple of 1024, at most 16384) whose stream and data images fit
 // the default 48 KB of shared memory -- 16384 for m = 2, 3 (BJ configs[0] is one CTA), 14336 for
