@@ -100,7 +100,8 @@ def test_c3_code_length_sweep_256mb(oracle, m):
 @pytest.mark.parametrize("m", [3, 4])
 def test_c3_table_decoders_with_double_errors(oracle, m):
     """configs[2] for the (7,4) / (15,11) table decoders that serve every
-    call >= 65 536 codewords, with 2-bit events (miscorrections) -- in full."""
+    call above the small-call limit (2 MiB coded), with 2-bit events
+    (miscorrections) -- in full."""
     n, _ = ham.code_nk(m)
     full_check(oracle, m, (256 << 20) * 8 // n, SEED ^ (m << 4) ^ 0x2B, 0.25, 0.25)
 

@@ -69,16 +69,20 @@ def test_every_received_word(oracle, m, N):
     assert_same(m, N, gpu_decode(m, rx, N), oracle.decode(m, rx, N))
 
 
+# calls of at most this many coded bits take the small-call decoder (hamming.cu kSmallCallBits);
+# larger ones the tile pipeline with the (7,4) / (15,11) / (31,26) table decoders
+SMALL_CALL_BITS = 1 << 24
+
+
 @pytest.mark.parametrize("m", [2, 3, 4])
 def test_every_received_word_tiled_large(oracle, m):
-    """Every received word of the code at N >= 2^17 codewords (a ragged tail
-    included), i.e. through the multi-CTA launches that serve every call of
-    >= 65 536 codewords -- the (7,4) / (15,11) table decoders for m = 3, 4.
-    Each block of 2^n words is a fresh permutation, so every word lands on
-    many codeword slots of a lane."""
+    """Every received word of the code at N above the small-call limit (a
+    ragged tail included), i.e. through the multi-CTA tile pipeline -- the
+    (7,4) / (15,11) table decoders for m = 3, 4.  Each block of 2^n words is
+    a fresh permutation, so every word lands on many codeword slots of a lane."""
     n = 2 ** m - 1
     rng = np.random.default_rng(1000 + m)
-    N = (1 << 17) + 77 if m < 4 else 4 * 2 ** n + 1234
+    N = max((1 << 17) + 77 if m < 4 else 4 * 2 ** n + 1234, SMALL_CALL_BITS // n + 77)
     blocks = (N + 2 ** n - 1) // 2 ** n
     words = np.concatenate([rng.permutation(2 ** n) for _ in range(blocks)]).astype(np.int64)[:N]
     bits = ((words[:, None] >> np.arange(n)) & 1).astype(np.uint8).reshape(-1)
@@ -87,11 +91,16 @@ def test_every_received_word_tiled_large(oracle, m):
 
 
 @pytest.mark.parametrize("m", [2, 3, 4, 5, 6, 7, 8])
-@pytest.mark.parametrize("N", [65535, 65536, 65537, 10 ** 6 + 13])
+@pytest.mark.parametrize("N", [65535, 65536, 65537, 10 ** 6 + 13, "small_max", "small_max+1"])
 def test_uniform_random_streams_large(oracle, m, N):
     """Uniformly random received bits (nearly every codeword erroneous, many
-    with several flips) with garbage in the input pad bits, on both sides of
-    the small-packet launch threshold and at 10^6 + 13 codewords."""
+    with several flips) with garbage in the input pad bits: around 65 536
+    codewords, at 10^6 + 13, and on both sides of the small-call limit (the
+    largest call the small-call decoder takes, and one codeword more: the
+    tile pipeline and, for m = 3..5, its table decoders)."""
+    n = 2 ** m - 1
+    if isinstance(N, str):
+        N = SMALL_CALL_BITS // n + (1 if N.endswith("+1") else 0)
     rng = np.random.default_rng(m * 7919 + N)
     rx = rng.integers(0, 256, ham.coded_bytes(m, N), dtype=np.uint8)
     assert_same(m, N, gpu_decode(m, rx, N), oracle.decode_mt(m, rx, N, THREADS))
