@@ -480,7 +480,8 @@ def run_sweeps(ham, torch, dev, peak):
     (device time, CUDA events on the launching stream), starting from an idle
     GPU (a 3 s pause after the sustained C5 run, 0.5 s between C3 points):
       c3: 256 MiB per call, every m, with and without syndromes -- median of
-          20 back-to-back calls alternating between two buffer sets (cold by
+          20 back-to-back calls alternating between two buffer sets, and the best
+          of 10 isolated calls (a queued ~100 us sleep ahead of each) (cold by
           size: 0.55-0.73 GB moved per call vs a 126 MB L2);
       c4: (31,26) 1 GiB, q2 = 0.25, every p -- median of 10 calls; the
           branch-free decoder should be flat in p ("spread");
@@ -531,6 +532,21 @@ def run_sweeps(ham, torch, dev, peak):
             row["us_per_call" + key] = round(t * 1e6, 2)
             row["coded_gbps" + key] = round(n * N / t / 1e9, 1)
             row["frac" + key] = round(alg(m, N, syn_on) / t / 1e9 / peak, 4)
+        # the same call in isolation: a ~100 us queued sleep ahead of each (host enqueue hidden,
+        # no back-to-back neighbour), best of 10
+        iso = []
+        for i in range(10):
+            rx, d, sy, c = sets[i & 1]
+            torch.cuda._sleep(200000)
+            a, b = ev(), ev()
+            a.record(st)
+            ham.decode(m, rx, N, data_out=d, syndromes=sy, corrected=c)
+            b.record(st)
+            iso.append((a, b))
+        torch.cuda.synchronize()
+        t = min(a.elapsed_time(b) for a, b in iso) / 1e3
+        row["us_isolated_best"] = round(t * 1e6, 2)
+        row["frac_isolated_best"] = round(alg(m, N, True) / t / 1e9 / peak, 4)
         pts.append(row)
         del sets
         time.sleep(0.5)
