@@ -2277,7 +2277,6 @@ HostSlotLayout host_slot_layout(int m, uint64_t chunk, int with_syn) {
 }
 
 #include "packets.cuh"
-#include "packets_fused.cuh"
 
 }  // namespace
 
@@ -2717,19 +2716,19 @@ hamming_status hamming_packet_launch_shape(uint32_t msg_bytes, int t, uint64_t r
   if (rc != HAMMING_OK) return rc;
   if (rx_stride % 16 != 0 || rx_stride < (g.coded_bits + 7) / 8)
     return set_err(HAMMING_E_ARG, "hamming_packet_launch_shape: rx_stride must be a multiple of 16 >= the coded bytes");
-  // the fused one-pass decoder (packets_fused.cuh), as hamming_decode_packets launches it
-  FusedGeom* F = new FusedGeom;
-  rc = fused_geom(g, rx_stride, std::min<uint64_t>(n_packets, 1ull << 31), sms, *F);
-  if (rc == HAMMING_OK) {
-    const uint64_t bytes = F->tab_bytes + static_cast<uint64_t>(F->warps) * F->warp_bytes;
-    if (warps) *warps = static_cast<int>(F->warps);
-    if (G) *G = static_cast<int>(F->G);
-    if (L) *L = static_cast<int>(F->L);
-    if (ctas) *ctas = static_cast<int>(std::min<uint64_t>(228ull * 1024 / (bytes + 1536), 32 / F->warps));
-    if (smem) *smem = static_cast<int>(bytes);
-  }
-  delete F;
-  return rc;
+  PacketTables T;
+  rc = build_packet_tables(g, T);
+  if (rc != HAMMING_OK) return rc;
+  BatchGeom bg;
+  rc = batch_geom(g, T, rx_stride, std::min<uint64_t>(n_packets, 1ull << 31), sms, bg);
+  if (rc != HAMMING_OK) return rc;
+  const uint64_t bytes = bg.tab_bytes + static_cast<uint64_t>(bg.warps) * bg.warp_bytes;
+  if (warps) *warps = static_cast<int>(bg.warps);
+  if (G) *G = static_cast<int>(bg.G);
+  if (L) *L = static_cast<int>(bg.L);
+  if (ctas) *ctas = static_cast<int>(std::min<uint64_t>(228ull * 1024 / (bytes + 1536), 32 / bg.warps));
+  if (smem) *smem = static_cast<int>(bytes);
+  return HAMMING_OK;
 }
 
 static hamming_status packet_common(uint32_t msg_bytes, int t, uint64_t pk_stride, const void* pk, PacketGeom& g,
@@ -2785,10 +2784,7 @@ hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void* rx_
   a.status = status_dev;
   a.counts = counts_dev;
   a.n_packets = n_packets;
-#ifdef HAM_PKT_TUNE  // tuning builds: the split (multi-pass) decoder on request, for A/B runs
-  if (getenv("HAM_PKT_SPLIT") != nullptr) return launch_packets_decode(g, a, st);
-#endif
-  return launch_packets_fused(g, a, st);
+  return launch_packets_decode(g, a, st);
 }
 
 hamming_status hamming_encode_packets(uint32_t msg_bytes, int t, const void* msg_dev, uint64_t msg_stride,
