@@ -1838,7 +1838,11 @@ struct Launcher {
     const uint64_t n_tiles = n_full + (rem > 0 ? 1 : 0);
     if (n_tiles > 0) {
       const uint64_t want = (n_tiles + WARPS - 1) / WARPS;
-      grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * bps));
+      int sms = sm_count(dev);
+#ifdef HAM_GRID_TUNE  // tuning builds only: the number of SMs the tile grid covers, from the environment
+      if (const char* ev = getenv("HAM_GRID_SMS")) sms = std::max(1, std::min(sms, atoi(ev)));
+#endif
+      grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sms) * bps));
     }
     const int store_count = (counter != nullptr && !accumulate && grid == 1) ? 1 : 0;
     // the slot: the count without a memset (multi-CTA launches) and the dynamic tail
