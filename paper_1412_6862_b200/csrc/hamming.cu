@@ -207,6 +207,22 @@ __device__ __forceinline__ void bulk_wait() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// A CTA-wide table copied from global memory by ONE TMA bulk copy (thread 0
+// issues it; the caller's other set-up runs meanwhile): cta_table_copy_begin,
+// then a __syncthreads, then cta_table_copy_wait on every thread.  `bar` is a
+// __shared__ mbarrier used once per launch.
+__device__ __forceinline__ void cta_table_copy_begin(void* dst, const void* src, uint32_t bytes, int tid, uint64_t* bar) {
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, bytes);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cta_table_copy_wait(uint64_t* bar) { mbar_wait(bar, 0); }
 __device__ __forceinline__ void st_global_cs_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
@@ -697,9 +713,8 @@ struct DecodeLut5Op {
   struct Args {};
 
   __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
-    const uint4* src = reinterpret_cast<const uint4*>(g_lut15raw);
-    uint4* dst = reinterpret_cast<uint4*>(sh);
-    for (int i = tid; i < 32768 * 2 / 16; i += nth) dst[i] = src[i];
+    __shared__ __align__(8) uint64_t tbar;
+    cta_table_copy_begin(sh, g_lut15raw, 32768 * 2, tid, &tbar);  // one TMA copy of the 64 KB table
     uint32_t* F = reinterpret_cast<uint32_t*>(sh + 32768 * 2);
     for (int e = tid; e < 32 * 32; e += nth) {  // F[s][lane] = the data bit of position s (0 if parity)
       const uint32_t v = (e >> 5) ? (1u << (e >> 5)) : 0u;  // a word with only position s set
@@ -708,6 +723,8 @@ struct DecodeLut5Op {
       for (int g = 1; g < 5; ++g) raw |= (v >> (g + 2)) & dmask(g);
       F[e] = raw;
     }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    cta_table_copy_wait(&tbar);
   }
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -748,10 +765,11 @@ struct DecodeLut4Op {
   static constexpr int SHARED = 32768 * 2;
   struct Args {};
 
-  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
-    const uint4* src = reinterpret_cast<const uint4*>(g_lut15);
-    uint4* dst = reinterpret_cast<uint4*>(sh);
-    for (int i = tid; i < SHARED / 16; i += nth) dst[i] = src[i];
+  __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int) {
+    __shared__ __align__(8) uint64_t tbar;
+    cta_table_copy_begin(sh, g_lut15, SHARED, tid, &tbar);  // one TMA copy of the 64 KB table
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    cta_table_copy_wait(&tbar);
   }
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -877,9 +895,8 @@ struct DecodeSecded4Op {
   __device__ __forceinline__ static uint32_t count1(const uint32_t (&sw)[8]) { return DecodeSecded3Op::count1(sw); }
 
   __device__ __forceinline__ static void cta_init(uint8_t* sh, int tid, int nth) {
-    const uint4* src = reinterpret_cast<const uint4*>(g_lut15);
-    uint4* dst = reinterpret_cast<uint4*>(sh);
-    for (int i = tid; i < 32768 * 2 / 16; i += nth) dst[i] = src[i];
+    __shared__ __align__(8) uint64_t tbar;
+    cta_table_copy_begin(sh, g_lut15, 32768 * 2, tid, &tbar);  // one TMA copy of the 64 KB table
     uint32_t* F = reinterpret_cast<uint32_t*>(sh + 32768 * 2);
     for (int e = tid; e < 16 * 32; e += nth) {  // F[s][lane] = the data bit of position s (0 if parity)
       const uint32_t v = (e >> 5) ? (1u << (e >> 5)) : 0u;
@@ -888,6 +905,8 @@ struct DecodeSecded4Op {
       for (int g = 1; g < 4; ++g) raw |= (v >> (g + 2)) & dmask(g);
       F[e] = raw;
     }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    cta_table_copy_wait(&tbar);
   }
 
   __device__ __forceinline__ static void lane(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
