@@ -2050,6 +2050,10 @@ constexpr uint64_t kSmallPacketCw = 1u << 16;
 // or, without a slot (graph capture), add into a count zeroed by a memset first.
 constexpr uint64_t kSmallCallBits = 1u << 24;  // 2 MiB of coded stream
 constexpr int kSmallCallThreads = 1024;
+#ifndef HAM_SMALL_PDL
+#define HAM_SMALL_PDL 1
+#endif
+constexpr int kSmallCallPdl = HAM_SMALL_PDL;  // programmatic dependent launch of small calls (0: plain launch)
 // codewords per CTA: the most (a multiple of 1024, at most 16384) whose stream and data images fit
 // the default 48 KB of shared memory -- 16384 for m = 2, 3 (BJ configs[0] is one CTA), 14336 for
 // m = 4, 6144 for m = 5, 3072 for m = 6
@@ -2069,6 +2073,11 @@ __global__ void __launch_bounds__(kSmallCallThreads)
   constexpr uint32_t n = Geo<M>::n, k = Geo<M>::k;
   extern __shared__ __align__(16) uint32_t small_sm[];
   __shared__ uint32_t cnt_s;  // 32-bit: a CTA holds at most 16384 codewords
+  // programmatic dependent launch: this grid may be resident before the previous kernel on the stream
+  // has finished (launch_small_decode sets the attribute); every global access waits for it here, and
+  // the next small call may start launching at once
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t c0 = blockIdx.x * CPB, nc = min(CPB, N - c0);
   // this CTA's stream: bits [c0 n, (c0 + nc) n), byte ib0 = c0 n / 8 (a multiple of 4)
   const uint32_t ib0 = c0 / 8 * n, in_bytes = min(in_total - ib0, (nc * n + 7) / 8 + 8);
@@ -2175,9 +2184,21 @@ hamming_status launch_small_decode(const uint8_t* in, uint64_t N, uint8_t* out, 
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(corrected)");
     }
   }
-  small_decode_kernel<M><<<grid, kSmallCallThreads, smem, st>>>(in, out, syn, static_cast<uint32_t>(N), ib, ob, counter,
-                                                                 accumulate ? 1 : 0, slot, CPB);
-  const cudaError_t e = cudaGetLastError();
+  // programmatic stream serialisation: back-to-back small calls (C1, graph-batched packets) overlap the
+  // next call's launch with this one's execution; the kernel's griddepcontrol.wait keeps stream order
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSmallCallThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = kSmallCallPdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, small_decode_kernel<M>, in, out, syn, static_cast<uint32_t>(N), ib, ob,
+                                     counter, accumulate ? 1 : 0, slot, CPB);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "small decode launch");
   g_launches = 1;
   g_grid = static_cast<int>(grid);
