@@ -283,3 +283,51 @@ def test_gpu_encoder_large_multi_round(oracle, m, secded):
     dec = res.data.cpu().numpy()[: ham.data_bytes(m, N)]
     assert np.array_equal(np.unpackbits(dec, bitorder="little")[: N * k],
                           np.unpackbits(data, bitorder="little")[: N * k])
+
+
+@pytest.mark.parametrize("m", [3, 4, 6])
+def test_chained_small_calls_keep_stream_order(oracle, m):
+    """Small calls launch with programmatic dependent launch: a call whose INPUT is the
+    previous call's OUTPUT (decode -> decode of the data stream as a new received stream, five deep,
+    eagerly and inside one CUDA graph) must still see the finished output, and each count stays its own."""
+    n, k = ham.code_nk(m)
+    N0 = 4681 if m == 3 else 2000
+    rx_np, _, _ = oracle.generate(m, 0xC4A1 + m, 0, N0, p=0.3, q2=0.2)
+    # oracle chain: level i decodes the previous level's data bytes as a packet of N_i codewords
+    want, cur, N = [], rx_np, N0
+    for _ in range(5):
+        wd, ws, wc = oracle.decode(m, cur, N)
+        want.append((N, wd, ws, wc))
+        N = wd.size * 8 // n
+        cur = wd
+    for mode in ("eager", "graph"):
+        bufs, N = [], N0
+        src = gpu(rx_np)
+        for (Ni, wd, _, _) in want:
+            bufs.append((src, Ni, torch.empty(ham.data_bytes(m, Ni), dtype=torch.uint8, device="cuda"),
+                         torch.empty(Ni, dtype=torch.uint8, device="cuda"), torch.empty(1, dtype=torch.int64, device="cuda")))
+            src = bufs[-1][2]
+        def run():
+            for s, Ni, d, sy, c in bufs:
+                ham.decode(m, s, Ni, data_out=d, syndromes=sy, corrected=c)
+        if mode == "eager":
+            run()
+        else:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                run()  # warm (tables, launch slots) outside capture
+                for _, _, d, sy, c in bufs:
+                    d.zero_(), sy.zero_(), c.zero_()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    run()
+            torch.cuda.synchronize()
+            for _, _, d, sy, c in bufs:
+                d.zero_(), sy.zero_(), c.fill_(-1)
+            g.replay()
+        torch.cuda.synchronize()
+        for (Ni, wd, ws, wc), (_, _, d, sy, c) in zip(want, bufs):
+            assert np.array_equal(d.cpu().numpy()[: wd.size], wd), (mode, m, Ni)
+            assert np.array_equal(sy.cpu().numpy(), ws), (mode, m, Ni)
+            assert int(c.item()) == wc, (mode, m, Ni)
