@@ -2815,11 +2815,7 @@ hamming_status hamming_decode_packets(uint32_t msg_bytes, int t, const void* rx_
           return set_err(HAMMING_E_OVERLAP, "hamming_decode_packets: buffers overlap");
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (counts_dev != nullptr) {
-    const cudaError_t e = cudaMemsetAsync(counts_dev, 0, 2 * sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counts)");
-  }
-  PacketArgs a{};
+  PacketArgs a{};  // counts: overwritten by the kernel itself (launch_packets_decode), no memset
   a.in = static_cast<const uint8_t*>(rx_dev);
   a.in_stride = rx_stride;
   a.out = static_cast<uint8_t*>(msg_dev);

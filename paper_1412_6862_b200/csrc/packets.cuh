@@ -170,6 +170,11 @@ struct PacketArgs {
   uint64_t seed, g_first, thresh;
   int all;
   uint8_t* gen_msg;    // generate: sent messages (nullable), msg_bytes apart
+  // decode counts without a memset: one CTA writes them (store_count), several publish through the
+  // stream's launch slot (the last CTA writes the total and resets the slot), else per-CTA atomics
+  // onto counts zeroed by the host; accumulate: add instead of overwrite (launches after the first)
+  LaunchSlot* slot;
+  int store_count, accumulate;
 };
 
 // Encoder / synthetic channel: one warp per packet (not on the hot path).
@@ -963,8 +968,25 @@ __global__ void __launch_bounds__(kPktWarps * 32)
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (cta_counts[0]) atomicAdd(&a.counts[0], cta_counts[0]);
-      if (cta_counts[1]) atomicAdd(&a.counts[1], cta_counts[1]);
+      if (a.store_count) {  // a single-CTA launch owns the counts
+        for (int i = 0; i < 2; ++i) a.counts[i] = (a.accumulate ? a.counts[i] : 0ull) + cta_counts[i];
+      } else if (a.slot != nullptr) {  // the last CTA to arrive publishes the totals and resets the slot
+        for (int i = 0; i < 2; ++i)
+          if (cta_counts[i]) atomicAdd(&a.slot->sum[i], cta_counts[i]);
+        __threadfence();
+        if (atomicAdd(&a.slot->done, 1u) == gridDim.x - 1) {
+          __threadfence();
+          for (int i = 0; i < 2; ++i) {
+            const unsigned long long tot = atomicExch(&a.slot->sum[i], 0ull);
+            a.counts[i] = (a.accumulate ? a.counts[i] : 0ull) + tot;
+          }
+          a.slot->claim = 0;
+          a.slot->done = 0;
+        }
+      } else {
+        if (cta_counts[0]) atomicAdd(&a.counts[0], cta_counts[0]);
+        if (cta_counts[1]) atomicAdd(&a.counts[1], cta_counts[1]);
+      }
     }
   }
 }
@@ -1012,6 +1034,11 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
   // the kernel's batch arithmetic is 32-bit: one launch per 2^31 packets (counts accumulate)
   constexpr uint64_t kMaxPackets = 1ull << 31;
   int launches = 0, grid = 0;
+  LaunchSlot* slot = (a.counts != nullptr) ? launch_slot(dev, st) : nullptr;
+  if (a.counts != nullptr && a.n_packets == 0) {  // nothing to decode: the counts are still overwritten
+    e = cudaMemsetAsync(a.counts, 0, 2 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counts)");
+  }
   for (uint64_t first = 0; first < a.n_packets; first += kMaxPackets) {
     PacketArgs c = a;
     c.n_packets = std::min(kMaxPackets, a.n_packets - first);
@@ -1022,6 +1049,13 @@ hamming_status launch_packets_decode(const PacketGeom& g, const PacketArgs& a, c
     const uint64_t batches = (c.n_packets + bg.G - 1) / bg.G;
     const uint64_t want = (batches + bg.warps - 1) / bg.warps;
     grid = static_cast<int>(std::min<uint64_t>(want, static_cast<uint64_t>(sm_count(dev)) * std::max(1, occ)));
+    c.accumulate = first > 0 ? 1 : 0;
+    c.store_count = grid == 1 ? 1 : 0;
+    c.slot = grid > 1 ? slot : nullptr;
+    if (a.counts != nullptr && grid > 1 && slot == nullptr && first == 0) {  // no slot (graph capture): memset + atomics
+      e = cudaMemsetAsync(a.counts, 0, 2 * sizeof(unsigned long long), st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(counts)");
+    }
     kfn<<<grid, bg.warps * 32, smem, st>>>(g, bg, c, T);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "packets decode launch");

@@ -184,3 +184,34 @@ def test_in_place_messages_with_word_and_byte_stores(M, t, msg_stride):
     assert np.array_equal(o[:, :M].reshape(-1), sent.cpu().numpy()[: P * M])
     assert (o[:, M:] == 0xA5).all()
     assert res.counts.cpu().tolist() == [P * t, 0] and bool((res.status[:P] == 1).all())
+
+
+def test_counts_overwritten_without_memset_eager_and_in_graph(oracle):
+    """The decoder writes its two counts itself (one CTA: stored; several: the last CTA publishes
+    through the stream's launch slot; under graph capture: memset + atomics) -- repeated calls
+    overwrite, never accumulate, on every path."""
+    M, t = 400, 5
+    stride = ham.packet_stride(M, t)
+    for P in (3, 5000):  # one CTA / many CTAs
+        rx_np, _ = oracle.generate_packets(M, t, 0xACE, 0, P, stride, p=0.6, want_msg=True)
+        _, ws, _ = oracle.decode_packets(M, t, rx_np, P, stride)
+        want = [int((ws != 0).sum()), 0]  # one flip per segment at most: every nonzero syndrome corrected
+        rx = torch.from_numpy(rx_np).cuda()
+        for _ in range(3):
+            res = ham.decode_packets(M, t, rx, P, rx_stride=stride)
+            torch.cuda.synchronize()
+            assert res.counts.cpu().tolist() == want, P
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            out = torch.empty(P * M, dtype=torch.uint8, device="cuda")
+            r0 = ham.decode_packets(M, t, rx, P, rx_stride=stride, msg_out=out, stream=side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                r1 = ham.decode_packets(M, t, rx, P, rx_stride=stride, msg_out=out, stream=side)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
+            torch.cuda.synchronize()
+            assert r1.counts.cpu().tolist() == want, ("graph", P)
+        assert r0.counts.cpu().tolist() == want
