@@ -13,7 +13,7 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tiles_kernel -s 4 -c 1 \
   -o $OUT/${TAG}_full_m6 -f python bench.py --config c3m6 --steps 1 --warmup 3 --no-e2e --no-cpu --no-sweeps \
   > $OUT/${TAG}_full_m6.log 2>&1
-for tool in initcheck memcheck; do
+for tool in ${SANITIZERS:-}; do  # compute-sanitizer is closed on the pool (exit 86); opt in with SANITIZERS="initcheck memcheck"
   echo "== $tool" >> $OUT/${TAG}_sanitizer.txt
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_workload.py $([ $tool = initcheck ] && echo --initcheck) \
     >> $OUT/${TAG}_sanitizer.txt 2>&1
