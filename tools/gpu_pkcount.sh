@@ -1,4 +1,5 @@
 #!/bin/bash
+# packet tests + the paper-grid bench after a packet-decoder change -> profiles/r02e_packets_bench.txt
 OUT=gpurun_out
 mkdir -p $OUT
 timeout 900 python -m pytest tests/test_gpu_packets.py tests/test_boundary_cpu.py -x -q > $OUT/pkc_pytest.log 2>&1; echo "rc=$?" >> $OUT/pkc_pytest.log; tail -2 $OUT/pkc_pytest.log
