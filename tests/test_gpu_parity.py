@@ -285,13 +285,14 @@ def test_gpu_encoder_large_multi_round(oracle, m, secded):
                           np.unpackbits(data, bitorder="little")[: N * k])
 
 
-@pytest.mark.parametrize("m", [3, 4, 6])
-def test_chained_small_calls_keep_stream_order(oracle, m):
+@pytest.mark.parametrize("m,N0", [(3, 4681), (4, 2000), (6, 2000), (4, 500_000), (6, 200_000)])
+def test_chained_small_calls_keep_stream_order(oracle, m, N0):
     """Small calls launch with programmatic dependent launch: a call whose INPUT is the
     previous call's OUTPUT (decode -> decode of the data stream as a new received stream, five deep,
     eagerly and inside one CUDA graph) must still see the finished output, and each count stays its own."""
     n, k = ham.code_nk(m)
-    N0 = 4681 if m == 3 else 2000
+    # N0 > one CTA's share (14336 / 3072 codewords for m = 4 / 6): multi-CTA small calls, whose count
+    # goes through the stream's launch slot eagerly and through a memset + atomics under capture
     rx_np, _, _ = oracle.generate(m, 0xC4A1 + m, 0, N0, p=0.3, q2=0.2)
     # oracle chain: level i decodes the previous level's data bytes as a packet of N_i codewords
     want, cur, N = [], rx_np, N0
